@@ -1,0 +1,287 @@
+#!/usr/bin/env python
+"""Benchmark of the GPipe hot path (BASELINE.json metric: training samples/sec, m = 32).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tgp|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N --steps K --warmup W
+
+Workload (BASELINE.json configs[1], "C2"): 32 pre-LN residual MLP blocks, width 4096 (GELU,
+LayerNorm), global batch 512, m = 32 micro-batches of 16 rows, checkpoint = except_last (the
+paper's default, P:108 / P:305 fn), bf16 operands with fp32 accumulation, plain SGD, MSE loss on
+synthetic N(0,1) data.  N GPUs = N partitions of 32/N blocks (one process per GPU, partitions
+connected through CUDA-IPC receive arenas); total work fixed -> "scaling": "strong".
+
+A step = tgp_forward + tgp_mse_loss_grad + tgp_backward + tgp_step (all GPipe tasks: F, F', B, W,
+copies, SGD).  `value` is timed with CUDA events on the device with inputs resident in HBM;
+`e2e` additionally copies x / target host->device (pinned) every step and reads the loss back.
+The 2.15 GB of bf16 weights streamed per step exceed the 126 MB L2, so no explicit L2 flush.
+`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BLOCKS, WIDTH, BATCH, M_CHUNKS = 32, 4096, 512, 32
+METRIC = "training samples/sec (m=32)"
+UNIT = "samples/s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown"]
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            p = [q.strip() for q in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, lrank
+
+
+def cpu_oracle_sample(steps=1, blocks=8, batch=BATCH, width=WIDTH):
+    """Time the fp64 oracle (as it stands) on a bounded sample of C2: `blocks` of the 32 blocks at full
+    width and full batch; returns (samples/s scaled to the full 32-block model, cores, description)."""
+    from oracle import model as OM
+    from synth import configs as C
+    from synth import gen as G
+
+    layers = C.resmlp_stack(blocks, width)
+    x, t = G.inputs(layers, batch, seed=1234, dtype="bf16")
+    params = G.params(layers, seed=1234, dtype="bf16")
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([int(i.get("num_threads", 0)) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        OM.train_step(layers, params, x, t, lr=0.05, m=M_CHUNKS, want_dx=False)
+        times.append(time.perf_counter() - t0)
+    per_step = statistics.median(times) * (BLOCKS / blocks)
+    desc = (f"oracle.model.train_step (numpy fp64) on {blocks} of the {BLOCKS} RESMLP blocks at width {width}, "
+            f"batch {batch}; median of {steps} step(s) scaled x{BLOCKS // blocks} to the full model")
+    return batch / per_step, cores, desc
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    v, cores, desc = cpu_oracle_sample(steps=max(1, args.steps), blocks=args.ref_blocks)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH / v,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(args.gpus),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config(n):
+    return {"workload": f"C2: {BLOCKS}-block pre-LN residual MLP (width {WIDTH}, GELU, LayerNorm), global batch "
+                        f"{BATCH}, m={M_CHUNKS}, checkpoint=except_last, plain SGD, MSE",
+            "global_batch": BATCH, "micro_batch_rows": BATCH // M_CHUNKS, "chunks": M_CHUNKS, "partitions": n,
+            "parallelism": f"pp{n}", "seq_len": None,
+            "l2": "no flush: 2.15 GB of bf16 weights streamed per step exceed the 126 MB L2"}
+
+
+def run_tgp(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2004_09910_b200 import Pipeline
+    from synth import configs as C
+
+    ws, rank, lrank = _dist()
+    n = ws
+    if args.gpus != n and ws > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {ws}")
+    if ws > 1:
+        dist.init_process_group("gloo")
+    torch.cuda.set_device(lrank)
+    dev = torch.device("cuda", lrank)
+    layers = C.resmlp_stack(BLOCKS, WIDTH)
+    devices = [-1] * n
+    devices[rank] = lrank
+    P = Pipeline(layers, chunks=M_CHUNKS, devices=devices, balance=[BLOCKS // n] * n, checkpoint=args.checkpoint,
+                 max_batch=BATCH, dtype="bf16", seed=1234)
+    if ws > 1:
+        from paper_2004_09910_b200.dist import connect_pipeline
+        connect_pipeline(P, rank, ws)
+    P.init_params(seed=1234)
+    first, last = rank == 0, rank == n - 1
+    g = torch.Generator(device="cpu").manual_seed(1234)
+    x_h = torch.randn(BATCH, WIDTH, generator=g).pin_memory()
+    t_h = torch.randn(BATCH, WIDTH, generator=g).pin_memory()
+    X = x_h.to(dev) if first else None
+    T = t_h.to(dev) if last else None
+    Y = torch.empty(BATCH, WIDTH, device=dev) if last else None
+    DY = torch.empty(BATCH, WIDTH, device=dev) if last else None
+
+    def step(e2e=False):
+        if e2e:
+            if first:
+                X.copy_(x_h, non_blocking=True)
+            if last:
+                T.copy_(t_h, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        P.forward(X, BATCH, Y)
+        loss = P.mse_loss_grad(Y, T, BATCH, DY) if last else None  # loss is read back to the host
+        P.backward(DY, None)
+        P.step(args.lr)
+        return loss
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(k, e2e):
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        k0 = P.kernel_count()
+        a.record()
+        losses = [step(e2e) for _ in range(k)]
+        b.record()
+        b.synchronize()
+        ms = a.elapsed_time(b)
+        nk = P.kernel_count() - k0
+        barrier()
+        if ws > 1:
+            from paper_2004_09910_b200.dist import max_over_ranks
+            ms = max_over_ranks(ms)
+        return ms, nk, losses
+
+    for _ in range(args.warmup):
+        step()
+    clk = ClockSampler(lrank)
+    clk.start()
+    ms, nk, losses = timed(args.steps, False)
+    clocks = clk.stop()
+    e2e_ms, _, _ = timed(args.steps, True)
+
+    # dominant kernel: forward weight-streaming GEMM, timed live on its stream (cycling cold weights)
+    gemm_ms, gemm_bytes, gemm_n = P.bench_dominant_gemm(rank, BATCH, reps=3)
+    peaks = _peaks()
+    if peaks and "hbm_gbs" in peaks:
+        peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    else:
+        peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    achieved = gemm_bytes / (gemm_ms * 1e-3) / 1e9
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        v, cores, desc = cpu_oracle_sample(steps=1, blocks=args.ref_blocks)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+    if rank == 0:
+        sps = BATCH * args.steps / (ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": sps, "unit": UNIT, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (N(0,1) inputs/targets, on-device U(+-1/sqrt(fan_in)) init)",
+            "config": _config(n),
+            "e2e": {"value": BATCH * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": 4 * BATCH * WIDTH * 2, "d2h_bytes_per_step": 8},
+            "gpu_launches": int(nk),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "kernel": "gemm_tc_kernel<16> forward W1 GEMM (M=16 rows, K=N=4096)",
+                         "algorithmic_bytes_per_launch": gemm_bytes, "avg_launch_us": gemm_ms * 1e3,
+                         "launches_timed": gemm_n, "peak_source": peak_src},
+            "clocks": clocks,
+            "loss_first_last": [losses[0], losses[-1]] if losses and losses[0] is not None else None,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    P.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tgp", choices=["tgp", "reference"])
+    ap.add_argument("--checkpoint", default="except_last", choices=["always", "except_last", "never"])
+    ap.add_argument("--lr", type=float, default=0.05)
+    ap.add_argument("--ref-blocks", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_tgp(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+/* tgp.h -- C ABI of the B200-native GPipe training library (arXiv 2004.09910, torchgpipe).
+ *
+ * The hot path (BASELINE.json north_star): synchronous GPipe pipeline-parallel training of a
+ * sequence of layers cut into n partitions, one partition per GPU; each mini-batch is cut into
+ * m micro-batches run on the deterministic clock-cycle schedule (§3.2.1 Alg. 1,
+ * m+n-1 forward clocks) and the mirrored backward, with checkpointed micro-batches
+ * recomputed (F'_{i,j}) right before B_{i,j} under the restored counter-based
+ * RNG, stage-to-stage activations / gradients / skip tensors moved by copy kernels on dedicated
+ * copy streams, weight gradients g^j = sum_i g_i^j computed by one
+ * deferred GEMM per weight, and a fused plain-SGD step.
+ *
+ * Conventions
+ *  - Every call returns tgp_status (0 = TGP_OK).  On failure the reason is available from
+ *    tgp_last_error() (thread-local, valid until the next failing call on the thread).
+ *  - Partitions are numbered j = 0..n_parts-1 in this ABI (the paper's j = 1..n).
+ *  - Matrices are row-major [rows][features], fp32, device memory unless stated "host".
+ *  - Calls are blocking: they return after all device work THIS PROCESS issued for the call has
+ *    completed (host timing around a call is valid; no hidden asynchronous state).
+ *  - A context is not thread-safe: one host thread drives it.
+ *  - No CPU fallback: a process without a usable sm_100 GPU gets TGP_E_CUDA / TGP_E_UNSUPPORTED
+ *    from tgp_create.  Pure host entry points (tgp_balance, tgp_split, tgp_schedule) need no GPU.
+ */
+#ifndef TGP_H
+#define TGP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TGP_OK = 0,
+  TGP_E_INVALID = -1,     /* bad argument, shape mismatch, bad balance / route        */
+  TGP_E_STATE = -2,       /* call out of order (backward before forward, ...)         */
+  TGP_E_CUDA = -3,        /* a CUDA runtime / driver call failed                      */
+  TGP_E_NOMEM = -4,       /* device allocation failed                                 */
+  TGP_E_UNSUPPORTED = -5, /* shape / device / feature not supported by this build     */
+  TGP_E_TIMEOUT = -6      /* a cross-partition handshake did not complete in time     */
+} tgp_status;
+
+/* Checkpoint policy (P:105, P:108, P:305 footnote; SURVEY reading Z4):
+ * ALWAYS every micro-batch recomputed; EXCEPT_LAST all but i = m (the paper's default);
+ * NEVER no recomputation (all activations kept). */
+typedef enum { TGP_CKPT_ALWAYS = 0, TGP_CKPT_EXCEPT_LAST = 1, TGP_CKPT_NEVER = 2 } tgp_checkpoint;
+
+/* Compute mode: FP32 = fp32 everything, SIMT FFMA GEMMs, no TF32 (reading Z16);
+ * BF16 = bf16 GEMM operands on tcgen05 tensor cores with fp32 accumulation; fp32 residual stream,
+ * LN statistics, messages, gradients and master weights (reading Z14). */
+typedef enum { TGP_FP32 = 0, TGP_BF16 = 1 } tgp_dtype;
+
+/* Layer kinds.  Parameters of layer l, in this order (canonical parameter index order):
+ *  TGP_LINEAR    y = act(x W^T + b) [dropout]          W [d_out][d_in], b [d_out]
+ *  TGP_RESMLP    y = x + W2 drop(act(W1 LN(x) + b1)) + b2, pre-LayerNorm (eps 1e-5), d_out == d_in
+ *                gamma [d_in], beta [d_in], W1 [d_hidden][d_in], b1 [d_hidden], W2 [d_out][d_hidden], b2 [d_out]
+ *  TGP_MERGE     y = act([x || s] W^T + b) [dropout], s = skip tensor popped from route pop_route
+ *                (concat-merge of a long skip connection)   W [d_out][d_in + d_skip], b [d_out]
+ *  TGP_BATCHNORM y = act(gamma (x - mu_i) / sqrt(var_i + 1e-5) + beta), statistics of micro-batch i
+ *                (P:56 footnote); running stats committed once per forward call from the whole
+ *                mini-batch (momentum 0.1, unbiased variance).   gamma [d], beta [d]   (FP32 mode only)
+ */
+typedef enum { TGP_LINEAR = 0, TGP_RESMLP = 1, TGP_MERGE = 2, TGP_BATCHNORM = 3 } tgp_kind;
+typedef enum { TGP_ACT_NONE = 0, TGP_ACT_RELU = 1, TGP_ACT_GELU = 2 } tgp_act;
+
+typedef struct {
+  int32_t kind;        /* tgp_kind */
+  int32_t d_in, d_out; /* feature widths (TGP_MERGE: d_in = width of x; d_skip comes from the route) */
+  int32_t d_hidden;    /* TGP_RESMLP hidden width, else 0 */
+  int32_t act;         /* tgp_act */
+  float dropout;       /* dropout probability after the activation (0 = none); Philox4x32-10 keyed by
+                          (seed, step), counter = (global element index >> 2, layer index, step) */
+  int32_t stash_route; /* route id whose skip tensor is this layer's OUTPUT, or -1 (@skippable stash) */
+  int32_t pop_route;   /* route id consumed at this layer's INPUT (TGP_MERGE), or -1 (pop) */
+} tgp_layer;
+
+typedef struct tgp_ctx tgp_ctx;
+
+/* ------------------------------------------------------------------ pure host entry points */
+
+/* Partition balancer ("partition whose pairwise resource discrepancy is small"; reading Z8):
+ * contiguous split of n_layers costs into n_parts non-empty blocks minimising the maximum block
+ * sum, ties broken by the lexicographically smallest boundary vector.  balance_out[n_parts]. */
+tgp_status tgp_balance(const double* layer_cost, int32_t n_layers, int32_t n_parts, int32_t* balance_out);
+
+/* Micro-batch split (reading Z7): sizes_out[m] = ceil(B/m) for the first B mod m
+ * micro-batches, floor(B/m) after.  TGP_E_INVALID unless 1 <= m <= B. */
+tgp_status tgp_split(int32_t B, int32_t m, int32_t* sizes_out);
+
+/* The clock-cycle schedule the runtime issues (Alg. 1 + mirrored backward + deferred dW), as
+ * 8-int32 records (phase, clock, kind, i, j, src, dst, route) with i, j 1-based:
+ * phase 0 forward / 1 backward / 2 weight-gradient; kind 0 F, 1 F' (recompute), 2 B, 3 COPY_F,
+ * 4 COPY_B, 5 SKIP_F, 6 SKIP_B, 7 W.  routes = n_routes (src, dst) partition pairs, 1-based.
+ * rec may be NULL to query the count; *n_rec receives the record count. */
+tgp_status tgp_schedule(int32_t m, int32_t n, tgp_checkpoint ckpt, const int32_t* routes, int32_t n_routes,
+                        int32_t* rec, int64_t cap, int64_t* n_rec);
+
+/* ------------------------------------------------------------------ context */
+
+/* Create a pipeline.  layers[n_layers] as above; balance[n_parts] layers per partition (NULL:
+ * tgp_balance on analytic per-layer costs); chunks = m; devices[n_parts]: CUDA ordinal hosting
+ * partition j in THIS process (repeats allowed: several partitions may share a GPU), or -1 when
+ * partition j is hosted by another process (multi-process pipeline: exchange tgp_ipc_export /
+ * tgp_ipc_import blobs, then tgp_connect).  max_batch bounds B of later calls; seed keys the
+ * dropout RNG.  All device memory (parameters, gradients, activation slots, receive buffers,
+ * stash) is allocated here; nothing is allocated on the step path.
+ * Errors: TGP_E_INVALID (chunks < 1, chunks > max_batch, sum(balance) != n_layers, a partition
+ * with 0 layers, n_parts > n_layers, shape mismatch between consecutive layers or along a route,
+ * pop before stash), TGP_E_UNSUPPORTED (bf16 widths not multiples of 128, BATCHNORM in bf16
+ * mode, no peer access between two local devices), TGP_E_NOMEM, TGP_E_CUDA. */
+tgp_status tgp_create(const tgp_layer* layers, int32_t n_layers, const int32_t* balance, int32_t n_parts,
+                      int32_t chunks, tgp_checkpoint ckpt, const int32_t* devices, int32_t max_batch,
+                      tgp_dtype dtype, uint64_t seed, tgp_ctx** out);
+void tgp_destroy(tgp_ctx* ctx);
+
+/* Multi-process pipelines: each local partition exports one opaque blob (its peer-visible
+ * receive arena as a CUDA IPC handle).  Every process imports the blobs of the remote partitions
+ * it exchanges data with (neighbours and skip-route peers; importing all is fine), then calls
+ * tgp_connect.  tgp_ipc_export: buf may be NULL to query *len. */
+tgp_status tgp_ipc_export(tgp_ctx* ctx, int32_t part, void* buf, int64_t cap, int64_t* len);
+tgp_status tgp_ipc_import(tgp_ctx* ctx, int32_t part, const void* buf, int64_t len);
+tgp_status tgp_connect(tgp_ctx* ctx);
+
+/* ------------------------------------------------------------------ training step */
+
+/* Forward pass F_{i,j} for all micro-batches on the clock-cycle schedule.
+ * x: [B][d_in] fp32 on devices[0] (required iff partition 0 is local, else NULL);
+ * y: [B][d_out] fp32 on devices[n-1] (required iff partition n-1 is local, else NULL).
+ * A forward discards the state of a previous forward that was not followed by backward. */
+tgp_status tgp_forward(tgp_ctx* ctx, const float* x, int32_t B, float* y);
+
+/* Loss on the gathered output -- library helper on the last partition's device:
+ * loss = sum (y - t)^2 / (B d_out), dy = 2 (y - t) / (B d_out).  loss_out: host, may be NULL. */
+tgp_status tgp_mse_loss_grad(tgp_ctx* ctx, const float* y, const float* target, int32_t B, float* dy,
+                             double* loss_out);
+
+/* Backward pass: mirrored clock-cycle, F'_{i,j} before B_{i,j} for checkpointed micro-batches,
+ * then the deferred weight-gradient task W_j.  dy: [B][d_out] fp32 on devices[n-1] (iff local);
+ * dx: [B][d_in] fp32 on devices[0] or NULL.  Gradients accumulate over forward/backward pairs
+ * until tgp_step.  TGP_E_STATE if no forward preceded it. */
+tgp_status tgp_backward(tgp_ctx* ctx, const float* dy, float* dx);
+
+/* Plain SGD on every local partition: theta <- theta - lr g (fp32 master; bf16 shadow refreshed),
+ * then gradients are logically reset.  Advances the dropout step counter. */
+tgp_status tgp_step(tgp_ctx* ctx, float lr);
+
+/* ------------------------------------------------------------------ parameters / introspection */
+
+/* Parameters in canonical order over ALL layers (see tgp_kind).  Only parameters of local
+ * partitions can be read / written (TGP_E_INVALID otherwise).  host buffers, fp32. */
+tgp_status tgp_num_params(tgp_ctx* ctx, int32_t* n);
+tgp_status tgp_param_info(tgp_ctx* ctx, int32_t idx, int32_t* layer, int32_t* part, int64_t* numel);
+tgp_status tgp_set_param(tgp_ctx* ctx, int32_t idx, const float* host);
+tgp_status tgp_get_param(tgp_ctx* ctx, int32_t idx, float* host);
+tgp_status tgp_get_grad(tgp_ctx* ctx, int32_t idx, float* host);
+/* Deterministic on-device initialisation of every local parameter (bench helper; W, b ~
+ * U(+-1/sqrt(fan_in)), gamma = 1, beta = 0). */
+tgp_status tgp_init_params(tgp_ctx* ctx, uint64_t seed);
+/* BatchNorm running statistics of layer `layer` (host [d] each). */
+tgp_status tgp_get_bn_running(tgp_ctx* ctx, int32_t layer, float* mean, float* var);
+
+/* The records this process actually issued in its last forward+backward, in issue order (same
+ * encoding as tgp_schedule; a multi-process context logs only records whose actor is local). */
+tgp_status tgp_get_issue_log(tgp_ctx* ctx, int32_t* rec, int64_t cap, int64_t* n_rec);
+
+/* Task timeline (enabled by tgp_set_trace(ctx, 1)): per executed compute task and copy, 6 int64
+ * (part, stream, kind, i, t0_ns, t1_ns), times from CUDA events relative to the start of the
+ * call on that partition's device (not comparable across devices). */
+tgp_status tgp_set_trace(tgp_ctx* ctx, int32_t on);
+tgp_status tgp_get_timeline(tgp_ctx* ctx, int64_t* rec, int64_t cap, int64_t* n_rec);
+
+/* Number of kernels this process launched (or replayed through CUDA graphs) since creation. */
+tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
+
+/* Runtime options: "graphs" (1 = capture each task's kernels into a CUDA graph; default 1),
+ * "pdl" (programmatic dependent launch between a task's kernels; default 1),
+ * "splitk" (0 = auto), "test_poison" (fill receive slots with NaN before each call, for the
+ * negative-control tests), "test_skip_wait" (drop the receive wait of partition `value`). */
+tgp_status tgp_set_option(tgp_ctx* ctx, const char* name, int64_t value);
+
+const char* tgp_last_error(void);
+
+/* Measurement helper (bench.py's roofline line): times the dominant kernel of the step -- the
+ * forward weight-streaming GEMM of every RESMLP/LINEAR layer of local partition `part`, launched
+ * exactly as F_{i,j} launches it for micro-batch 1 of a batch of B rows -- cycling through the
+ * partition's layers (cold weights) `reps` rounds, with CUDA events on the partition's compute
+ * stream.  *ms: average ms per launch; *bytes: average algorithmic bytes per launch (weights +
+ * activation operand + epilogue reads/writes); *launches: launches timed. */
+tgp_status tgp_bench_dominant_gemm(tgp_ctx* ctx, int32_t part, int32_t B, int32_t reps, double* ms, double* bytes,
+                                   int64_t* launches);
+
+/* ------------------------------------------------------------------ kernel-level test entry */
+
+/* D[m][n] = sum_k A[m][k] B[n][k] on the tcgen05 path (bf16 in, fp32 out).
+ * a_mn: A stored [K][M] (else [M][K]); b_mn: B stored [K][N] (else [N][K]).
+ * D layout: b_mn == 1 -> row-major [M][N] (the weight-gradient orientation); b_mn == 0 -> [N][M]
+ * (activation orientation: row n, feature m -- the swap-AB skinny path).  splits: split-K
+ * cluster size (0 = auto).  Device pointers; stream = cudaStream_t or NULL; synchronous.  Used by
+ * the kernel unit tests and micro-benchmarks. */
+tgp_status tgp_test_gemm_bf16(const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,
+                              int32_t a_mn, int32_t b_mn, int32_t splits, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGP_H */

@@ -1,0 +1,350 @@
+// tcgen05 / TMA bf16 GEMM kernel (see gemm_tc.cuh for the design) and its host launcher.
+#include <algorithm>
+#include <cstdlib>
+
+#include "epilogue.cuh"
+#include "gemm_tc.cuh"
+#include "host.h"
+#include "kernels.h"
+
+namespace tgp {
+
+template <int BN>
+struct TcCfg {
+  static constexpr int BK = 64;
+  static constexpr int A_BYTES = 128 * BK * 2;  // 16 KB
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int BUDGET = 196608;
+  static constexpr int STAGES = (BUDGET / STAGE) > 12 ? 12 : (BUDGET / STAGE);
+  static constexpr int BNP = BN + 1;  // odd pitch: conflict-free partial-tile smem
+  static constexpr int RED_BYTES = 128 * BNP * 4;
+  static constexpr int DATA = (STAGES * STAGE > RED_BYTES) ? STAGES * STAGE : RED_BYTES;
+  static constexpr int SMEM = DATA + 1024 + 256;
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+                   const __grid_constant__ CUtensorMap tmB1, const GemmParams p) {
+  using C = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tile = blockIdx.x, n_tile = blockIdx.z;
+  const int nkb_total = p.K / C::BK;
+  const int kb0 = blockIdx.y * p.kb_per_split;
+  const int kb1 = min(kb0 + p.kb_per_split, nkb_total);
+  const int nkb = kb1 > kb0 ? kb1 - kb0 : 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB0);
+    tma_prefetch_desc(&tmB1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_launch();
+
+  auto stage_a = [&](int s) { return smem + s * C::STAGE; };
+  auto stage_b = [&](int s) { return smem + s * C::STAGE + C::A_BYTES; };
+  const int m0 = m_tile * 128;
+  const int nb = n_tile * BN;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // ---------------- TMA producer
+      const uint64_t pol_a = p.a_is_weight ? policy_evict_first() : policy_evict_last();
+      const uint64_t pol_b = policy_evict_last();
+      auto load_a = [&](int s, int kb) {
+        const int k = kb * C::BK;
+        if (A_MN) {
+          tma_load_2d(&tmA, &full[s], stage_a(s), m0, k, pol_a);
+          tma_load_2d(&tmA, &full[s], stage_a(s) + 8192, m0 + 64, k, pol_a);
+        } else {
+          tma_load_2d(&tmA, &full[s], stage_a(s), k, m0, pol_a);
+        }
+      };
+      auto load_b = [&](int s, int kb) {
+        const int k = kb * C::BK;
+        const bool second = k >= p.k_seg;
+        const CUtensorMap* tm = second ? &tmB1 : &tmB0;
+        const int kk = second ? k - p.k_seg : k;
+        if (B_MN) {
+#pragma unroll
+          for (int c = 0; c < BN / 64; ++c) tma_load_2d(tm, &full[s], stage_b(s) + c * 8192, p.n0 + nb + c * 64, kk, pol_b);
+        } else {
+          tma_load_2d(tm, &full[s], stage_b(s), kk, p.n0 + nb, pol_b);
+        }
+      };
+      int pre = 0;
+      if (p.a_is_weight) {
+        // weights do not depend on the previous kernel: start streaming them before the wait
+        pre = nkb < C::STAGES ? nkb : C::STAGES;
+        for (int it = 0; it < pre; ++it) {
+          mbar_arrive_expect_tx(&full[it], C::STAGE);
+          load_a(it, kb0 + it);
+        }
+      }
+      griddep_wait();
+      for (int it = 0; it < pre; ++it) load_b(it, kb0 + it);
+      for (int it = pre; it < nkb; ++it) {
+        const int s = it % C::STAGES, r = it / C::STAGES;
+        mbar_wait(&empty[s], (r & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], C::STAGE);
+        load_a(s, kb0 + it);
+        load_b(s, kb0 + it);
+      }
+    }
+    // reconverge before the .aligned cluster barriers below (only one lane ran the producer loop)
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      // ---------------- MMA issuer (single thread)
+      constexpr uint32_t idesc = make_idesc_bf16(128, BN, A_MN, B_MN);
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % C::STAGES, r = it / C::STAGES;
+        mbar_wait(&full[s], r & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(stage_a(s));
+        const uint32_t b_base = smem_u32(stage_b(s));
+#pragma unroll
+        for (int kk = 0; kk < C::BK / 16; ++kk) {
+          const uint64_t ad = A_MN ? make_sdesc_sw128(a_base + kk * 2048, 8192, 1024)
+                                   : make_sdesc_sw128(a_base + kk * 32, 16, 1024);
+          const uint64_t bd = B_MN ? make_sdesc_sw128(b_base + kk * 2048, 8192, 1024)
+                                   : make_sdesc_sw128(b_base + kk * 32, 16, 1024);
+          tc_mma_bf16(tmem, ad, bd, idesc, (it | kk) != 0);
+        }
+        tc_commit(&empty[s]);
+      }
+      if (nkb > 0)
+        tc_commit(tfull);
+      else
+        mbar_arrive(tfull);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue warps 2..5: TMEM -> registers
+    griddep_wait();
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int lg = warp & 3;  // TMEM lane group accessible to this warp
+    const int fl = lg * 32 + lane;
+    const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
+    if (p.epi.mode == EPI_DW) {
+      const EpiParams& e = p.epi;
+      const int m = m0 + fl;
+      float* row = e.dw + (int64_t)m * e.ldw + nb;
+#pragma unroll 1
+      for (int c = 0; c < BN / 16; ++c) {
+        float v[16];
+        tmem_ld16(taddr + c * 16, v);
+        if (nkb == 0) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        }
+        if (nb + c * 16 < p.N && m < p.M) {
+          float4* dst = reinterpret_cast<float4*>(row + c * 16);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            if (e.accumulate) {
+              float4 old = dst[q];
+              o.x += old.x;
+              o.y += old.y;
+              o.z += old.z;
+              o.w += old.w;
+            }
+            dst[q] = o;
+          }
+        }
+      }
+    } else {
+      float* red = reinterpret_cast<float*>(smem);
+#pragma unroll 1
+      for (int c = 0; c < BN / 16; ++c) {
+        float v[16];
+        tmem_ld16(taddr + c * 16, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) red[fl * C::BNP + c * 16 + i] = nkb ? v[i] : 0.0f;
+      }
+    }
+  }
+  tc_fence_before();
+
+  if (p.epi.mode != EPI_DW) {
+    // ---------------- deterministic split-K reduction through DSMEM, fixed rank order
+    cluster_sync();
+    const int S = gridDim.y;
+    const int rank = (int)cluster_ctarank();
+    const int rpr = 128 / S;
+    const int et = (int)threadIdx.x - 64;
+    if (et >= 0 && et < rpr) {
+      const int fl = rank * rpr + et;
+      const int f = m0 + fl;
+      const int nvalid = min(BN, p.N - nb);
+      const uint32_t base = smem_u32(smem) + (uint32_t)(fl * C::BNP) * 4u;
+      uint32_t rb[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) rb[q] = q < S ? mapa_shared(base, (uint32_t)q) : 0u;
+      float csum = 0.0f;
+#pragma unroll 1
+      for (int n = 0; n < nvalid; ++n) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < S) acc += ld_dsmem_f32(rb[q] + 4u * (uint32_t)n);
+        if (f < p.M) csum += epi_apply(p.epi, f, nb + n, acc);
+      }
+      if (p.epi.mode == EPI_ACT_BWD && p.epi.colsum && f < p.M) p.epi.colsum[f] = csum;
+    }
+    cluster_sync();
+  }
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------------- host side
+static bool make_map(CUtensorMap* map, const TcMat& t, int box_inner, int box_outer) {
+  const Driver* d = driver();
+  if (!d) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)t.cols, (cuuint64_t)t.rows};
+  cuuint64_t strides[1] = {(cuuint64_t)t.ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = d->tensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(t.ptr), dims,
+                                       strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld box=%dx%d", (int)r,
+              (long long)t.rows, (long long)t.cols, (long long)t.ld, box_inner, box_outer);
+    return false;
+  }
+  return true;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch_tc(cudaStream_t st, bool pdl, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
+                     const GemmParams& p, int S, int ntiles) {
+  using C = TcCfg<BN>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) {
+      set_error("cudaFuncSetAttribute(smem=%d): %s", C::SMEM, cudaGetErrorString(e));
+      return -3;
+    }
+    attr_done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.M / 128, S, ntiles);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 1;
+  attrs[0].val.clusterDim.y = S;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = pdl ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b0, b1, p);
+  if (e != cudaSuccess) {
+    set_error("gemm_tc launch (BN=%d A_MN=%d B_MN=%d grid=%d,%d,%d): %s", BN, (int)A_MN, (int)B_MN, p.M / 128, S,
+              ntiles, cudaGetErrorString(e));
+    return -3;
+  }
+  return 0;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B0, const TcMat* B1, bool b_mn,
+            GemmParams p, int splits) {
+  if (p.M % 128 || p.K % 64 || p.M <= 0 || p.N <= 0) {
+    set_error("gemm_tc: unsupported shape M=%d N=%d K=%d (need M%%128==0, K%%64==0)", p.M, p.N, p.K);
+    return -5;
+  }
+  const bool dw = p.epi.mode == EPI_DW;
+  int BN;
+  if (dw) {
+    BN = p.N >= 256 ? 256 : (p.N >= 128 ? 128 : 64);
+    if (p.N % 64 && b_mn) {
+      set_error("gemm_tc dW: N=%d must be a multiple of 64", p.N);
+      return -5;
+    }
+  } else {
+    BN = p.N <= 16 ? 16 : p.N <= 32 ? 32 : p.N <= 64 ? 64 : p.N <= 128 ? 128 : 256;
+  }
+  const int ntiles = (p.N + BN - 1) / BN;
+  const int nkb = p.K / 64;
+  int S = 1;
+  if (!dw) {
+    const int mt = p.M / 128;
+    S = splits > 0 ? splits : env_int("TGP_SPLITK", 0);
+    if (S <= 0) {
+      S = (148 + mt * ntiles / 2) / (mt * ntiles);
+    }
+    S = std::max(1, std::min(S, 8));
+    S = std::min(S, nkb);
+    while (128 % S) --S;  // rows-per-rank must divide the 128-row tile
+  }
+  p.kb_per_split = (nkb + S - 1) / S;
+  S = (nkb + p.kb_per_split - 1) / p.kb_per_split;
+  while (128 % S) {  // keep 128 divisible by S after re-balancing
+    ++p.kb_per_split;
+    S = (nkb + p.kb_per_split - 1) / p.kb_per_split;
+  }
+  if (!B1) p.k_seg = p.K;
+
+  CUtensorMap ma, mb0, mb1;
+  if (!make_map(&ma, A, 64, a_mn ? 64 : 128)) return -3;
+  const int b_outer = b_mn ? 64 : BN;
+  if (!make_map(&mb0, B0, 64, b_outer)) return -3;
+  if (B1) {
+    if (!make_map(&mb1, *B1, 64, b_outer)) return -3;
+  } else {
+    mb1 = mb0;
+  }
+#define TGP_LAUNCH(BNv)                                                                    \
+  if (BN == BNv) {                                                                         \
+    if (!a_mn && !b_mn) return launch_tc<BNv, false, false>(st, pdl, ma, mb0, mb1, p, S, ntiles); \
+    if (a_mn && !b_mn) return launch_tc<BNv, true, false>(st, pdl, ma, mb0, mb1, p, S, ntiles);   \
+    if (a_mn && b_mn) return launch_tc<BNv, true, true>(st, pdl, ma, mb0, mb1, p, S, ntiles);     \
+  }
+  if (!dw) {
+    TGP_LAUNCH(16)
+    TGP_LAUNCH(32)
+  }
+  TGP_LAUNCH(64)
+  TGP_LAUNCH(128)
+  TGP_LAUNCH(256)
+#undef TGP_LAUNCH
+  set_error("gemm_tc: no instantiation for BN=%d a_mn=%d b_mn=%d", BN, (int)a_mn, (int)b_mn);
+  return -5;
+}
+
+}  // namespace tgp

@@ -1,0 +1,753 @@
+// tgp runtime: context creation, buffers, peer arenas (CUDA IPC), clock-cycle issue of tasks,
+// copy-stream transport with flag handshakes, task executors (F / F' / B / W), SGD, ABI entry
+// points.  PAPER.md references: Alg. 1 P:148-167 (clock cycle), P:103-108 (device order,
+// checkpointing), P:198-203 (copy streams), P:212 (checkpoint slot shared with the receive
+// buffer), P:242-245 (portals: one direct copy per skip tensor), P:70 (g = sum_i g_i), P:307 (SGD).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <memory>
+#include <mutex>
+
+#include "host.h"
+#include "runtime.h"
+
+using namespace tgp;
+
+// ============================================================================ errors / driver
+namespace tgp {
+static thread_local std::string g_err;
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+const char* get_error() { return g_err.c_str(); }
+
+const Driver* driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn)
+      d.tensorMapEncodeTiled = (decltype(d.tensorMapEncodeTiled))fn;
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess && fn)
+      d.streamWaitValue32 = (decltype(d.streamWaitValue32))fn;
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess && fn)
+      d.streamWriteValue32 = (decltype(d.streamWriteValue32))fn;
+    d.ok = d.tensorMapEncodeTiled && d.streamWaitValue32 && d.streamWriteValue32;
+  });
+  if (!d.ok) {
+    set_error("CUDA driver entry points unavailable (no GPU driver?)");
+    return nullptr;
+  }
+  return &d;
+}
+
+void* Pool::get(size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  if (bytes == 0) bytes = 256;
+  if (bytes > left) {
+    const size_t cs = std::max(bytes, size_t(256) << 20);
+    void* p = nullptr;
+    if (cudaMalloc(&p, cs) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, cs) != cudaSuccess) return nullptr;
+    chunks.push_back(p);
+    cur = (char*)p;
+    left = cs;
+  }
+  void* r = cur;
+  cur += bytes;
+  left -= bytes;
+  return r;
+}
+void Pool::release() {
+  for (void* p : chunks) cudaFree(p);
+  chunks.clear();
+  cur = nullptr;
+  left = 0;
+}
+}  // namespace tgp
+
+// ============================================================================ helpers
+static int op_size(const tgp_ctx* c) { return c->bf16 ? 2 : 4; }
+static inline uint32_t* flag_fwd(const ArenaView& v, int i) { return v.flags + (i - 1); }
+static inline uint32_t* flag_grad(const tgp_ctx* c, const ArenaView& v, int i) { return v.flags + c->m + (i - 1); }
+static inline uint32_t* flag_skip(const tgp_ctx* c, const ArenaView& v, int r, int i) {
+  return v.flags + 2 * c->m + r * c->m + (i - 1);
+}
+static inline uint32_t* flag_dskip(const tgp_ctx* c, const ArenaView& v, int r, int i) {
+  return v.flags + 2 * c->m + (int)c->routes.size() * c->m + r * c->m + (i - 1);
+}
+static inline uint32_t* flag_done(const tgp_ctx* c, const ArenaView& v, int from_part) {
+  return v.flags + 2 * c->m + 2 * (int)c->routes.size() * c->m + from_part;
+}
+static int n_flags(const tgp_ctx* c) { return 2 * c->m + 2 * (int)c->routes.size() * c->m + c->n; }
+
+static int part_d_in(const tgp_ctx* c, int j) { return c->layers[c->part_l0[j]].L.d_in; }
+static int part_d_out(const tgp_ctx* c, int j) { return c->layers[c->part_l0[j + 1] - 1].L.d_out; }
+
+static ArenaLayout make_layout(const tgp_ctx* c, int j) {
+  ArenaLayout a;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    size_t r = off;
+    off += (b + 255) & ~size_t(255);
+    return r;
+  };
+  a.off_fwd = take((size_t)c->max_batch * part_d_in(c, j) * 4);
+  a.off_grad = take((size_t)c->max_batch * part_d_out(c, j) * 4);
+  a.off_skip.assign(c->routes.size(), SIZE_MAX);
+  a.off_dskip.assign(c->routes.size(), SIZE_MAX);
+  for (const Route& r : c->routes) {
+    if (r.dst == j) a.off_skip[r.id] = take((size_t)c->max_batch * r.width * op_size(c));
+    if (r.src == j && r.dst != j) a.off_dskip[r.id] = take((size_t)c->max_batch * r.width * 4);
+  }
+  a.off_flags = take((size_t)n_flags(c) * 4);
+  a.bytes = off;
+  return a;
+}
+
+static ArenaView make_view(const tgp_ctx* c, int j, char* base) {
+  const ArenaLayout& a = c->layout[j];
+  ArenaView v;
+  v.fwd_in = (float*)(base + a.off_fwd);
+  v.grad_in = (float*)(base + a.off_grad);
+  v.skip_in.assign(c->routes.size(), nullptr);
+  v.dskip_in.assign(c->routes.size(), nullptr);
+  for (size_t r = 0; r < c->routes.size(); ++r) {
+    if (a.off_skip[r] != SIZE_MAX) v.skip_in[r] = base + a.off_skip[r];
+    if (a.off_dskip[r] != SIZE_MAX) v.dskip_in[r] = (float*)(base + a.off_dskip[r]);
+  }
+  v.flags = (uint32_t*)(base + a.off_flags);
+  return v;
+}
+
+// dropout threshold: keep iff (word >> 8) >= ceil(p * 2^24)  <=>  (word >> 8) * 2^-24 >= p
+static uint32_t drop_thresh(float p) {
+  if (p <= 0.0f) return 0u;
+  const double t = std::ceil((double)p * 16777216.0);
+  return (uint32_t)std::max(1.0, std::min(t, 16777216.0));
+}
+
+// ============================================================================ GEMM dispatch
+namespace {
+struct Opnd {
+  const void* p;
+  int64_t rows, cols, ld;
+};
+}  // namespace
+
+// D[m][n] = sum_k A(m,k) B(n,k);  a_mn: A memory [K][M], else [M][K];  b_mn: B memory [K][N] else [rows][K]
+static int run_gemm(tgp_ctx* c, Stage& s, bool pdl, Opnd A, bool a_mn, Opnd B0, const Opnd* B1, bool b_mn, int M,
+                    int N, int K, int n0, int k_seg, bool a_weight, const EpiParams& e) {
+  GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.n0 = n0;
+  p.k_seg = B1 ? k_seg : K;
+  p.a_is_weight = a_weight ? 1 : 0;
+  p.epi = e;
+  c->kernels += 1;
+  if (c->bf16) {
+    TcMat a{A.p, A.rows, A.cols, A.ld}, b0{B0.p, B0.rows, B0.cols, B0.ld};
+    TcMat b1 = B1 ? TcMat{B1->p, B1->rows, B1->cols, B1->ld} : b0;
+    const int Kp = (K + 63) / 64 * 64;
+    p.K = Kp;
+    if (B1 && k_seg % 64) {
+      set_error("merge: d_in=%d must be a multiple of 64 in bf16 mode", k_seg);
+      return TGP_E_UNSUPPORTED;
+    }
+    return gemm_tc(s.comp, pdl && c->use_pdl, a, a_mn, b0, B1 ? &b1 : nullptr, b_mn, p, c->splitk);
+  }
+  SimtOperand sa = a_mn ? SimtOperand{(const float*)A.p, 1, A.ld} : SimtOperand{(const float*)A.p, A.ld, 1};
+  SimtOperand sb0 = b_mn ? SimtOperand{(const float*)B0.p, 1, B0.ld} : SimtOperand{(const float*)B0.p, B0.ld, 1};
+  SimtOperand sb1{nullptr, 0, 0};
+  if (B1) sb1 = b_mn ? SimtOperand{(const float*)B1->p, 1, B1->ld} : SimtOperand{(const float*)B1->p, B1->ld, 1};
+  return gemm_simt(s.comp, pdl && c->use_pdl, sa, sb0, sb1, p);
+}
+
+static const void* wparam(tgp_ctx* c, Stage& s, const LayerRT& L, int k) {
+  if (c->bf16) return s.shadow + L.poff[k];
+  return s.master + L.poff[k];
+}
+static float* mparam(Stage& s, const LayerRT& L, int k) { return s.master + L.poff[k]; }
+static float* gparam(Stage& s, const LayerRT& L, int k) { return s.grad + L.poff[k]; }
+
+static char* opptr(tgp_ctx* c, void* base, int64_t row, int64_t w) {
+  return (char*)base + (size_t)row * w * op_size(c);
+}
+
+// skip operand destination for route r at the stash side (global row r0)
+static void* stash_dst(tgp_ctx* c, Stage& s, int r, int64_t r0) {
+  const Route& R = c->routes[r];
+  void* base = (R.dst == s.j) ? s.self.skip_in[r] : s.skip_send[r];
+  return opptr(c, base, r0, R.width);
+}
+
+// ============================================================================ task executors
+// F_{i,j} (and F'_{i,j}: identical kernels and launch configuration -> bitwise identical output)
+static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
+  const int slot = c->slot_of[i];
+  float* x = s.self.fwd_in + (size_t)r0 * s.d_in;
+  bool first_kernel = true;
+  auto pdl = [&]() {
+    bool r = !first_kernel;
+    first_kernel = false;
+    return r;
+  };
+  for (int l = s.l0; l < s.l1; ++l) {
+    LayerRT& L = c->layers[l];
+    const int din = L.L.d_in, dout = L.L.d_out;
+    float* y = (l == s.l1 - 1) ? s.out + (size_t)r0 * dout : L.out[slot];
+    EpiParams e{};
+    e.op_bf16 = c->bf16 ? 1 : 0;
+    e.seed = c->seed;
+    e.step = s.dstep;
+    e.site = (uint32_t)l;
+    e.row_global0 = r0;
+    switch (L.L.kind) {
+      case TGP_LINEAR:
+      case TGP_MERGE: {
+        TGP_TRY(convert_rows(s.comp, pdl() && c->use_pdl, x, din, M, din, opptr(c, L.Xop, r0, din), din, c->bf16,
+                             nullptr));
+        c->kernels++;
+        e.mode = EPI_LINEAR_FWD;
+        e.act = L.L.act;
+        e.bias = mparam(s, L, 1);
+        e.zbuf = (L.L.act != TGP_ACT_NONE) ? L.z[slot] : nullptr;
+        e.ldz = dout;
+        e.out0 = y;
+        e.ld0 = dout;
+        e.drop_thresh = drop_thresh(L.L.dropout);
+        e.drop_scale = L.L.dropout > 0 ? 1.0f / (1.0f - L.L.dropout) : 1.0f;
+        e.drop_width = dout;
+        if (L.L.stash_route >= 0) {
+          e.op = stash_dst(c, s, L.L.stash_route, r0);
+          e.ld_op = dout;
+        }
+        const int K = din + L.d_skip;
+        Opnd A{wparam(c, s, L, 0), dout, K, K};
+        Opnd B0{L.Xop, c->max_batch, din, din};
+        if (L.L.kind == TGP_MERGE) {
+          const Route& R = c->routes[L.L.pop_route];
+          Opnd B1{s.self.skip_in[R.id], c->max_batch, R.width, R.width};
+          TGP_TRY(run_gemm(c, s, pdl(), A, false, B0, &B1, false, dout, M, K, r0, din, true, e));
+        } else {
+          TGP_TRY(run_gemm(c, s, pdl(), A, false, B0, nullptr, false, dout, M, K, r0, K, true, e));
+        }
+        break;
+      }
+      case TGP_RESMLP: {
+        const int H = L.L.d_hidden;
+        TGP_TRY(ln_fwd(s.comp, pdl() && c->use_pdl, x, din, M, din, mparam(s, L, 0), mparam(s, L, 1),
+                       opptr(c, L.Hop, r0, din), din, c->bf16, L.mean[slot], L.rstd[slot]));
+        c->kernels++;
+        EpiParams e1 = e;
+        e1.mode = EPI_LINEAR_FWD;
+        e1.act = L.L.act;
+        e1.bias = mparam(s, L, 3);
+        e1.zbuf = L.z[slot];
+        e1.ldz = H;
+        e1.op = opptr(c, L.Gop, r0, H);
+        e1.ld_op = H;
+        e1.drop_thresh = drop_thresh(L.L.dropout);
+        e1.drop_scale = L.L.dropout > 0 ? 1.0f / (1.0f - L.L.dropout) : 1.0f;
+        e1.drop_width = H;
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 2), H, din, din}, false,
+                         Opnd{L.Hop, c->max_batch, din, din}, nullptr, false, H, M, din, r0, din, true, e1));
+        EpiParams e2 = e;
+        e2.mode = EPI_RESID_FWD;
+        e2.bias = mparam(s, L, 5);
+        e2.res = x;
+        e2.ld_res = din;
+        e2.out0 = y;
+        e2.ld0 = dout;
+        if (L.L.stash_route >= 0) {
+          e2.op = stash_dst(c, s, L.L.stash_route, r0);
+          e2.ld_op = dout;
+        }
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 4), dout, H, H}, false, Opnd{L.Gop, c->max_batch, H, H},
+                         nullptr, false, dout, M, H, r0, H, true, e2));
+        break;
+      }
+      case TGP_BATCHNORM: {
+        const size_t so = (size_t)(i - 1) * din;
+        TGP_TRY(bn_fwd(s.comp, x, M, din, mparam(s, L, 0), mparam(s, L, 1), L.L.act, y, L.z[slot], L.bn_mu + so,
+                       L.bn_rstd + so, L.bn_var + so));
+        c->kernels++;
+        first_kernel = false;
+        if (L.L.stash_route >= 0) {
+          TGP_TRY(convert_rows(s.comp, false, y, dout, M, dout, stash_dst(c, s, L.L.stash_route, r0), dout, c->bf16,
+                               nullptr));
+          c->kernels++;
+        }
+        break;
+      }
+    }
+    x = y;
+  }
+  return 0;
+}
+
+// B_{i,j}: VJPs through the partition's layers in reverse; stashes dW operands, per-micro-batch
+// column partials (bias / LN / BN grads), writes dx rows (message source) and skip gradients.
+static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
+  const int slot = c->slot_of[i];
+  float* g = s.self.grad_in + (size_t)r0 * s.d_out;
+  int pp = 0;
+  bool first_kernel = true;
+  auto pdl = [&]() {
+    bool r = !first_kernel;
+    first_kernel = false;
+    return r;
+  };
+  for (int l = s.l1 - 1; l >= s.l0; --l) {
+    LayerRT& L = c->layers[l];
+    const int din = L.L.d_in, dout = L.L.d_out;
+    const float* xin = (l == s.l0) ? s.self.fwd_in + (size_t)r0 * s.d_in : c->layers[l - 1].out[slot];
+    float* dx = (l == s.l0) ? s.dx_out + (size_t)r0 * s.d_in : s.gbuf[pp];
+    pp ^= 1;
+    if (L.L.stash_route >= 0) {  // add the skip gradient of the portal (reverse direction)
+      const Route& R = c->routes[L.L.stash_route];
+      const float* ds = (R.dst == s.j) ? s.dskip_local[R.id] : s.self.dskip_in[R.id] + (size_t)r0 * R.width;
+      TGP_TRY(add_rows(s.comp, pdl() && c->use_pdl, g, ds, (int64_t)M * dout));
+      c->kernels++;
+    }
+    const size_t po = (size_t)(i - 1);
+    EpiParams e{};
+    e.op_bf16 = c->bf16 ? 1 : 0;
+    e.seed = c->seed;
+    e.step = s.dstep;
+    e.site = (uint32_t)l;
+    e.row_global0 = r0;
+    switch (L.L.kind) {
+      case TGP_LINEAR:
+      case TGP_MERGE: {
+        const float th_p = L.L.dropout;
+        TGP_TRY(act_bwd_rows(s.comp, pdl() && c->use_pdl, g, L.z[slot], M, dout, L.L.act, drop_thresh(th_p),
+                             th_p > 0 ? 1.0f / (1.0f - th_p) : 1.0f, c->seed, s.dstep, (uint32_t)l, r0,
+                             opptr(c, L.Zop, r0, dout), dout, c->bf16, L.pb + po * dout));
+        c->kernels++;
+        const int K = din + L.d_skip;
+        e.mode = EPI_STORE;
+        e.out0 = dx;
+        e.ld0 = din;
+        e.split_f = din;
+        if (L.L.kind == TGP_MERGE) {
+          const Route& R = c->routes[L.L.pop_route];
+          e.out1 = (R.src == s.j) ? s.dskip_local[R.id] : s.dskip_send[R.id] + (size_t)r0 * R.width;
+          e.ld1 = R.width;
+        }
+        // dx^T[m = in][n] = sum_k W[k = out][m] dZ[n][k]
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 0), dout, K, K}, true, Opnd{L.Zop, c->max_batch, dout, dout},
+                         nullptr, false, K, M, dout, r0, dout, true, e));
+        break;
+      }
+      case TGP_RESMLP: {
+        const int H = L.L.d_hidden;
+        TGP_TRY(convert_rows(s.comp, pdl() && c->use_pdl, g, dout, M, dout, opptr(c, L.dYop, r0, dout), dout, c->bf16,
+                             L.pb2 + po * dout));
+        c->kernels++;
+        EpiParams e1 = e;
+        e1.mode = EPI_ACT_BWD;
+        e1.act = L.L.act;
+        e1.zbuf = L.z[slot];
+        e1.ldz = H;
+        e1.op = opptr(c, L.dAop, r0, H);
+        e1.ld_op = H;
+        e1.colsum = L.pb + po * H;
+        e1.drop_thresh = drop_thresh(L.L.dropout);
+        e1.drop_scale = L.L.dropout > 0 ? 1.0f / (1.0f - L.L.dropout) : 1.0f;
+        e1.drop_width = H;
+        // dg^T[m = hidden][n] = sum_k W2[k = out][m] dY[n][k]
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 4), dout, H, H}, true, Opnd{L.dYop, c->max_batch, dout, dout},
+                         nullptr, false, H, M, dout, r0, dout, true, e1));
+        EpiParams e2 = e;
+        e2.mode = EPI_STORE;
+        e2.out0 = s.dh;
+        e2.ld0 = din;
+        e2.split_f = din;
+        // dh^T[m = in][n] = sum_k W1[k = hidden][m] dA[n][k]
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 2), H, din, din}, true, Opnd{L.dAop, c->max_batch, H, H},
+                         nullptr, false, din, M, H, r0, H, true, e2));
+        TGP_TRY(ln_bwd(s.comp, pdl() && c->use_pdl, s.dh, xin, L.mean[slot], L.rstd[slot], mparam(s, L, 0), g, dx, M,
+                       din, L.pg + po * din, L.pbt + po * din));
+        c->kernels += 2;
+        break;
+      }
+      case TGP_BATCHNORM: {
+        TGP_TRY(bn_bwd(s.comp, g, xin, L.z[slot], L.bn_mu + po * din, L.bn_rstd + po * din, mparam(s, L, 0), M, din,
+                       L.L.act, dx, L.pg + po * din, L.pb + po * din));
+        c->kernels++;
+        first_kernel = false;
+        break;
+      }
+    }
+    g = dx;
+  }
+  return 0;
+}
+
+// W_j: deferred weight gradients g^j = sum_i g_i^j as one GEMM per weight over the stacked
+// micro-batches, plus fixed-order reductions of the per-micro-batch column partials.
+static int exec_wgrad(tgp_ctx* c, Stage& s, int B) {
+  const bool acc = !s.grads_fresh;
+  for (int l = s.l0; l < s.l1; ++l) {
+    LayerRT& L = c->layers[l];
+    const int din = L.L.d_in, dout = L.L.d_out;
+    EpiParams e{};
+    e.mode = EPI_DW;
+    e.accumulate = acc ? 1 : 0;
+    switch (L.L.kind) {
+      case TGP_LINEAR:
+      case TGP_MERGE: {
+        const int K = din + L.d_skip;
+        e.dw = gparam(s, L, 0);
+        e.ldw = K;
+        // dW[m = out][n = in] = sum_k dZ[k][m] X[k][n]
+        TGP_TRY(run_gemm(c, s, false, Opnd{L.Zop, B, dout, dout}, true, Opnd{L.Xop, B, din, din}, nullptr, true, dout,
+                         din, B, 0, B, false, e));
+        if (L.L.kind == TGP_MERGE) {
+          const Route& R = c->routes[L.L.pop_route];
+          e.dw = gparam(s, L, 0) + din;
+          TGP_TRY(run_gemm(c, s, false, Opnd{L.Zop, B, dout, dout}, true, Opnd{s.self.skip_in[R.id], B, R.width, R.width},
+                           nullptr, true, dout, R.width, B, 0, B, false, e));
+        }
+        TGP_TRY(reduce_partials(s.comp, L.pb, c->m, dout, gparam(s, L, 1), acc));
+        c->kernels++;
+        break;
+      }
+      case TGP_RESMLP: {
+        const int H = L.L.d_hidden;
+        e.dw = gparam(s, L, 2);
+        e.ldw = din;
+        TGP_TRY(run_gemm(c, s, false, Opnd{L.dAop, B, H, H}, true, Opnd{L.Hop, B, din, din}, nullptr, true, H, din, B, 0,
+                         B, false, e));
+        e.dw = gparam(s, L, 4);
+        e.ldw = H;
+        TGP_TRY(run_gemm(c, s, false, Opnd{L.dYop, B, dout, dout}, true, Opnd{L.Gop, B, H, H}, nullptr, true, dout, H, B,
+                         0, B, false, e));
+        TGP_TRY(reduce_partials(s.comp, L.pg, c->m, din, gparam(s, L, 0), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pbt, c->m, din, gparam(s, L, 1), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pb, c->m, H, gparam(s, L, 3), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pb2, c->m, dout, gparam(s, L, 5), acc));
+        c->kernels += 4;
+        break;
+      }
+      case TGP_BATCHNORM: {
+        TGP_TRY(reduce_partials(s.comp, L.pg, c->m, din, gparam(s, L, 0), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pb, c->m, din, gparam(s, L, 1), acc));
+        c->kernels += 2;
+        break;
+      }
+    }
+  }
+  s.grads_fresh = false;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------- task graphs
+// Each task's kernel sequence is captured once into a CUDA graph (per micro-batch, per batch size)
+// and replayed: one host launch per task instead of ~3 per layer.
+template <typename Fn>
+static int run_task(tgp_ctx* c, Stage& s, TaskGraph& tg, int B, Fn&& fn) {
+  if (!c->use_graphs) return fn();
+  if (tg.exec && tg.B == B) {
+    TGP_CUDA_TRY(cudaGraphLaunch(tg.exec, s.comp));
+    c->kernels += tg.kernels;
+    return 0;
+  }
+  if (tg.exec) {
+    cudaGraphExecDestroy(tg.exec);
+    tg.exec = nullptr;
+  }
+  const int64_t k0 = c->kernels;
+  TGP_CUDA_TRY(cudaStreamBeginCapture(s.comp, cudaStreamCaptureModeThreadLocal));
+  int rc = fn();
+  cudaGraph_t graph = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(s.comp, &graph);
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  TGP_CUDA_TRY(ce);
+  ce = cudaGraphInstantiate(&tg.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  TGP_CUDA_TRY(ce);
+  tg.B = B;
+  tg.kernels = c->kernels - k0;
+  c->kernels = k0;
+  TGP_CUDA_TRY(cudaGraphLaunch(tg.exec, s.comp));
+  c->kernels += tg.kernels;
+  return 0;
+}
+
+// ============================================================================ waits / transport
+static int wait_flag(tgp_ctx* c, cudaStream_t st, uint32_t* flag, uint32_t v) {
+  const Driver* d = driver();
+  if (!d) return TGP_E_CUDA;
+  unsigned flags = CU_STREAM_WAIT_VALUE_GEQ;
+  if (c->can_flush) flags |= CU_STREAM_WAIT_VALUE_FLUSH;
+  TGP_CU_TRY(d->streamWaitValue32((CUstream)st, (CUdeviceptr)flag, v, flags));
+  return 0;
+}
+
+static void trace_begin(tgp_ctx* c, Stage& s, cudaStream_t st, int stream_id, int kind, int i, cudaEvent_t* a) {
+  if (!c->trace) return;
+  cudaEventCreate(a);
+  cudaEventRecord(*a, st);
+  (void)s;
+  (void)stream_id;
+  (void)kind;
+  (void)i;
+}
+static void trace_end(tgp_ctx* c, Stage& s, cudaStream_t st, int stream_id, int kind, int i, cudaEvent_t a) {
+  if (!c->trace) return;
+  cudaEvent_t b;
+  cudaEventCreate(&b);
+  cudaEventRecord(b, st);
+  c->trace_recs.push_back(TraceRec{s.j, stream_id, kind, i, a, b});
+}
+
+static void micro_rows(const tgp_ctx* c, int B, int i, int* r0, int* M) {
+  const int q = B / c->m, r = B % c->m;
+  const int ii = i - 1;
+  *r0 = ii * q + std::min(ii, r);
+  *M = q + (ii < r ? 1 : 0);
+}
+
+// partitions that push data into partition j (receive arena writers)
+static std::vector<int> writers_of(const tgp_ctx* c, int j) {
+  std::vector<int> w;
+  if (j > 0) w.push_back(j - 1);
+  if (j + 1 < c->n) w.push_back(j + 1);
+  for (const Route& r : c->routes) {
+    if (r.src == r.dst) continue;
+    if (r.dst == j) w.push_back(r.src);
+    if (r.src == j) w.push_back(r.dst);
+  }
+  std::sort(w.begin(), w.end());
+  w.erase(std::unique(w.begin(), w.end()), w.end());
+  return w;
+}
+
+// Issue one schedule record whose actor is local.  Copies ride on the producer's copy streams and
+// end with a flag release on the consumer; computes wait on their receive flags on the compute
+// stream (the consumer never blocks the producer).
+static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>>& first_push) {
+  const int i = rc.i;
+  int r0 = 0, M = 0;
+  if (i > 0) micro_rows(c, B, i, &r0, &M);
+  const uint32_t seq = c->seq;
+  switch (rc.kind) {
+    case K_COPY_F:
+    case K_COPY_B:
+    case K_SKIP_F:
+    case K_SKIP_B: {
+      const int src = rc.src - 1, dst = rc.dst - 1;
+      Stage* sp = c->local[src];
+      if (!sp) return 0;  // actor is the source; remote source -> nothing to issue here
+      Stage& s = *sp;
+      const bool skip = rc.kind == K_SKIP_F || rc.kind == K_SKIP_B;
+      cudaStream_t st = skip ? s.cskip : s.cact;
+      cudaEvent_t ev = (rc.kind == K_COPY_F || rc.kind == K_SKIP_F) ? s.fdone[i - 1] : s.bdone[i - 1];
+      TGP_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+      if (!first_push[src][dst]) {
+        // the consumer must have finished the previous call before its receive slots are reused
+        TGP_TRY(wait_flag(c, st, flag_done(c, s.self, dst), seq - 1));
+        first_push[src][dst] = 1;
+      }
+      const ArenaView& pv = c->view[dst];
+      cudaEvent_t ta = nullptr;
+      trace_begin(c, s, st, skip ? 2 : 1, rc.kind, i, &ta);
+      uint32_t* ctr = s.counters + (skip ? 1 : 0);
+      if (rc.kind == K_COPY_F) {
+        TGP_TRY(push_rows(st, s.out + (size_t)r0 * s.d_out, pv.fwd_in + (size_t)r0 * s.d_out, false,
+                          (int64_t)M * s.d_out, ctr, flag_fwd(pv, i), seq));
+      } else if (rc.kind == K_COPY_B) {
+        TGP_TRY(push_rows(st, s.dx_out + (size_t)r0 * s.d_in, pv.grad_in + (size_t)r0 * s.d_in, false,
+                          (int64_t)M * s.d_in, ctr, flag_grad(c, pv, i), seq));
+      } else if (rc.kind == K_SKIP_F) {
+        const Route& R = c->routes[rc.route];
+        const int64_t nb = (int64_t)M * R.width * op_size(c);
+        TGP_TRY(push_bytes(st, opptr(c, s.skip_send[R.id], r0, R.width), opptr(c, pv.skip_in[R.id], r0, R.width), nb, ctr,
+                           flag_skip(c, pv, R.id, i), seq));
+      } else {
+        const Route& R = c->routes[rc.route];
+        TGP_TRY(push_rows(st, s.dskip_send[R.id] + (size_t)r0 * R.width, pv.dskip_in[R.id] + (size_t)r0 * R.width,
+                          false, (int64_t)M * R.width, ctr, flag_dskip(c, pv, R.id, i), seq));
+      }
+      c->kernels++;
+      trace_end(c, s, st, skip ? 2 : 1, rc.kind, i, ta);
+      c->issue_log.push_back(rc);
+      return 0;
+    }
+    case K_F:
+    case K_RECOMPUTE:
+    case K_B: {
+      const int j = rc.j - 1;
+      Stage* sp = c->local[j];
+      if (!sp) return 0;
+      Stage& s = *sp;
+      if (rc.kind == K_F && j > 0 && c->skip_wait_part != j) TGP_TRY(wait_flag(c, s.comp, flag_fwd(s.self, i), seq));
+      if (rc.kind == K_F)
+        for (const Route& R : c->routes)
+          if (R.dst == j && R.src != j) TGP_TRY(wait_flag(c, s.comp, flag_skip(c, s.self, R.id, i), seq));
+      if (rc.kind == K_B) {
+        if (j < c->n - 1 && c->skip_wait_part != j) TGP_TRY(wait_flag(c, s.comp, flag_grad(c, s.self, i), seq));
+        for (const Route& R : c->routes)
+          if (R.src == j && R.dst != j) TGP_TRY(wait_flag(c, s.comp, flag_dskip(c, s.self, R.id, i), seq));
+      }
+      cudaEvent_t ta = nullptr;
+      trace_begin(c, s, s.comp, 0, rc.kind, i, &ta);
+      if (rc.kind == K_B) {
+        TGP_TRY(run_task(c, s, s.gB[i - 1], B, [&] { return exec_backward(c, s, i, r0, M); }));
+        TGP_CUDA_TRY(cudaEventRecord(s.bdone[i - 1], s.comp));
+      } else {
+        TGP_TRY(run_task(c, s, s.gF[i - 1], B, [&] { return exec_forward(c, s, i, r0, M); }));
+        if (rc.kind == K_F) TGP_CUDA_TRY(cudaEventRecord(s.fdone[i - 1], s.comp));
+      }
+      trace_end(c, s, s.comp, 0, rc.kind, i, ta);
+      c->issue_log.push_back(rc);
+      return 0;
+    }
+    case K_W: {
+      const int j = rc.j - 1;
+      Stage* sp = c->local[j];
+      if (!sp) return 0;
+      Stage& s = *sp;
+      cudaEvent_t ta = nullptr;
+      trace_begin(c, s, s.comp, 0, rc.kind, 0, &ta);
+      // the W graph bakes in the accumulate flag -> only replay when grads are fresh
+      if (s.grads_fresh) {
+        TGP_TRY(run_task(c, s, s.gW, B, [&] { return exec_wgrad(c, s, B); }));
+        s.grads_fresh = false;
+      } else {
+        TGP_TRY(exec_wgrad(c, s, B));
+      }
+      trace_end(c, s, s.comp, 0, rc.kind, 0, ta);
+      c->issue_log.push_back(rc);
+      return 0;
+    }
+  }
+  return 0;
+}
+
+static int finish_call(tgp_ctx* c) {
+  // tell every partition that writes into a local partition that this call is done on it
+  for (int j = 0; j < c->n; ++j) {
+    Stage* sp = c->local[j];
+    if (!sp) continue;
+    for (int k : writers_of(c, j)) {
+      TGP_TRY(signal_flag(sp->comp, flag_done(c, c->view[k], j), c->seq));
+      c->kernels++;
+    }
+  }
+  for (int j = 0; j < c->n; ++j) {
+    Stage* sp = c->local[j];
+    if (!sp) continue;
+    TGP_CUDA_TRY(cudaSetDevice(sp->dev));
+    TGP_CUDA_TRY(cudaStreamSynchronize(sp->comp));
+    TGP_CUDA_TRY(cudaStreamSynchronize(sp->cact));
+    TGP_CUDA_TRY(cudaStreamSynchronize(sp->cskip));
+  }
+  if (c->trace) {
+    for (auto& t : c->trace_recs) {
+      Stage* s = c->local[t.part];
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, s->ev_start, t.a);
+      cudaEventElapsedTime(&b, s->ev_start, t.b);
+      int64_t rec[6] = {t.part, t.stream, t.kind, t.i, (int64_t)(a * 1e6), (int64_t)(b * 1e6)};
+      c->timeline.insert(c->timeline.end(), rec, rec + 6);
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+    c->trace_recs.clear();
+  }
+  return 0;
+}
+
+static int begin_call(tgp_ctx* c) {
+  c->seq++;
+  for (int j = 0; j < c->n; ++j) {
+    Stage* sp = c->local[j];
+    if (!sp) continue;
+    TGP_CUDA_TRY(cudaSetDevice(sp->dev));
+    TGP_CUDA_TRY(cudaEventRecord(sp->ev_start, sp->comp));
+    // copy streams must not run ahead of the call's start (events of the previous call)
+    TGP_CUDA_TRY(cudaStreamWaitEvent(sp->cact, sp->ev_start, 0));
+    TGP_CUDA_TRY(cudaStreamWaitEvent(sp->cskip, sp->ev_start, 0));
+  }
+  return 0;
+}
+
+// ============================================================================ ABI
+extern "C" {
+
+const char* tgp_last_error(void) { return get_error(); }
+
+tgp_status tgp_balance(const double* cost, int32_t L, int32_t n, int32_t* out) {
+  if (!cost || !out || L < 1 || n < 1 || n > L) {
+    set_error("tgp_balance: need 1 <= n_parts <= n_layers");
+    return TGP_E_INVALID;
+  }
+  std::vector<int> tmp(n);
+  if (!balance_minmax(cost, L, n, tmp.data())) {
+    set_error("tgp_balance failed");
+    return TGP_E_INVALID;
+  }
+  for (int j = 0; j < n; ++j) out[j] = tmp[j];
+  return TGP_OK;
+}
+
+tgp_status tgp_split(int32_t B, int32_t m, int32_t* sizes) {
+  if (!sizes || m < 1 || m > B) {
+    set_error("tgp_split: need 1 <= m <= B (m=%d B=%d)", m, B);
+    return TGP_E_INVALID;
+  }
+  std::vector<int> t(m);
+  split_sizes(B, m, t.data());
+  for (int i = 0; i < m; ++i) sizes[i] = t[i];
+  return TGP_OK;
+}
+
+tgp_status tgp_schedule(int32_t m, int32_t n, tgp_checkpoint ckpt, const int32_t* routes, int32_t n_routes,
+                        int32_t* rec, int64_t cap, int64_t* n_rec) {
+  if (m < 1 || n < 1 || (int)ckpt < 0 || (int)ckpt > 2 || n_routes < 0 || (n_routes > 0 && !routes)) {
+    set_error("tgp_schedule: bad arguments");
+    return TGP_E_INVALID;
+  }
+  std::vector<std::pair<int, int>> r;
+  for (int q = 0; q < n_routes; ++q) {
+    if (routes[2 * q] < 1 || routes[2 * q + 1] < routes[2 * q] || routes[2 * q + 1] > n) {
+      set_error("tgp_schedule: route %d must satisfy 1 <= src <= dst <= n", q);
+      return TGP_E_INVALID;
+    }
+    r.emplace_back(routes[2 * q], routes[2 * q + 1]);
+  }
+  auto recs = emit_schedule(m, n, (int)ckpt, r);
+  if (n_rec) *n_rec = (int64_t)recs.size();
+  if (rec) {
+    if (cap < (int64_t)recs.size()) {
+      set_error("tgp_schedule: cap %lld < %zu records", (long long)cap, recs.size());
+      return TGP_E_INVALID;
+    }
+    memcpy(rec, recs.data(), recs.size() * sizeof(Rec));
+  }
+  return TGP_OK;
+}
+
+}  // extern "C"
+
+#include "runtime_create.inc"

@@ -1,0 +1,132 @@
+// Runtime data structures of a tgp context (host side).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tgp.h"
+#include "kernels.h"
+#include "plan.h"
+
+namespace tgp {
+
+// Device bump allocator (zero-initialised chunks).
+struct Pool {
+  int dev = 0;
+  std::vector<void*> chunks;
+  char* cur = nullptr;
+  size_t left = 0;
+  void* get(size_t bytes);
+  void release();
+};
+
+struct Route {
+  int id = -1;
+  int stash_layer = -1, pop_layer = -1;
+  int src = -1, dst = -1;  // 0-based partitions
+  int width = 0;
+};
+
+// Pointers into a partition's peer-visible receive arena, valid in THIS process.
+struct ArenaView {
+  float* fwd_in = nullptr;            // [max_batch][d_in]  fp32: stage input (= checkpoint slot)
+  float* grad_in = nullptr;           // [max_batch][d_out] fp32: incoming output gradient
+  std::vector<void*> skip_in;         // per route with dst == part: [max_batch][w] op dtype
+  std::vector<float*> dskip_in;       // per route with src == part (src != dst): [max_batch][w] fp32
+  uint32_t* flags = nullptr;          // see flag_* helpers
+};
+
+struct ArenaLayout {
+  size_t off_fwd = 0, off_grad = 0, off_flags = 0, bytes = 0;
+  std::vector<size_t> off_skip, off_dskip;  // indexed by route id, SIZE_MAX when absent
+};
+
+struct LayerRT {
+  tgp_layer L{};
+  int idx = 0, part = 0, d_skip = 0;
+  int nparam = 0, pidx0 = 0;
+  int64_t poff[6] = {0}, pnum[6] = {0};
+  // deferred-dW operand stash (global rows, op dtype, max_batch rows)
+  void *Xop = nullptr, *Zop = nullptr, *Hop = nullptr, *Gop = nullptr, *dAop = nullptr, *dYop = nullptr;
+  // per-micro-batch column partials [m][w] fp32
+  float *pb = nullptr, *pb2 = nullptr, *pg = nullptr, *pbt = nullptr;
+  // per activation slot (checkpoint-managed): layer output, pre-activation, LN stats
+  std::vector<float*> out, z, mean, rstd;
+  // BatchNorm per micro-batch statistics [m][d] and running stats [d]
+  float *bn_mu = nullptr, *bn_var = nullptr, *bn_rstd = nullptr, *bn_rm = nullptr, *bn_rv = nullptr;
+};
+
+struct TaskGraph {
+  cudaGraphExec_t exec = nullptr;
+  int B = -1;
+  int64_t kernels = 0;
+};
+
+struct Stage {
+  int j = 0, dev = 0, l0 = 0, l1 = 0, d_in = 0, d_out = 0, maxw = 0;
+  cudaStream_t comp = nullptr, cact = nullptr, cskip = nullptr;
+  std::vector<cudaEvent_t> fdone, bdone;
+  cudaEvent_t ev_start = nullptr;
+  std::vector<cudaEvent_t> tr_ev;  // timeline events (pairs)
+  Pool pool;
+  void* arena = nullptr;
+  ArenaView self;
+  float* out = nullptr;     // [max_batch][d_out] stage output (message source)
+  float* dx_out = nullptr;  // [max_batch][d_in] input gradient (message source)
+  std::vector<void*> skip_send;     // route id -> [max_batch][w] op dtype (src side, cross routes)
+  std::vector<float*> dskip_send;   // route id -> [max_batch][w] fp32 (dst side, cross routes)
+  std::vector<float*> dskip_local;  // route id -> [mb_cap][w] fp32 (src == dst)
+  float *master = nullptr, *grad = nullptr;
+  __nv_bfloat16* shadow = nullptr;
+  int64_t n_elems = 0;
+  float* dh = nullptr;
+  float* gbuf[2] = {nullptr, nullptr};
+  uint32_t* counters = nullptr;  // [8]
+  double* loss_buf = nullptr;
+  int* bn_rows = nullptr;
+  uint32_t* dstep = nullptr;  // device copy of the optimizer step (dropout counter)
+  std::vector<TaskGraph> gF, gB;
+  TaskGraph gW;
+  bool grads_fresh = true;
+};
+
+struct TraceRec {
+  int part, stream, kind, i;
+  cudaEvent_t a, b;
+};
+
+}  // namespace tgp
+
+struct tgp_ctx {
+  std::vector<tgp::LayerRT> layers;
+  std::vector<tgp::Route> routes;
+  std::vector<int> balance, devices, part_l0;
+  int n = 0, m = 0, ckpt = 1, max_batch = 0, mb_cap = 0, nslots = 1;
+  bool bf16 = false;
+  uint64_t seed = 0;
+  uint32_t step = 0;
+  uint32_t seq = 0;
+  int state = 0;  // 0 created, 1 forwarded, 2 backwarded
+  int cur_B = 0;
+  std::vector<tgp::Stage*> local;       // by partition (nullptr if remote)
+  std::vector<tgp::ArenaView> view;     // by partition
+  std::vector<tgp::ArenaLayout> layout; // by partition
+  std::vector<void*> imported;          // IPC mappings to close
+  std::vector<tgp::Rec> fwd_recs, bwd_recs, w_recs;
+  std::vector<tgp::Rec> issue_log;
+  std::vector<int> slot_of;  // 1-based micro-batch -> slot
+  int64_t kernels = 0;
+  // options
+  bool use_graphs = true, use_pdl = true, trace = false, poison = false;
+  int splitk = 0, skip_wait_part = -1;
+  bool can_flush = false;
+  std::vector<tgp::TraceRec> trace_recs;
+  std::vector<int64_t> timeline;
+  std::vector<std::pair<int, int>> route_parts_1b;
+  bool connected = true;
+  int n_params = 0;
+  std::vector<int> param_layer, param_local;
+};

@@ -1,0 +1,283 @@
+"""Thin ctypes binding of the tgp C ABI (include/tgp.h).  Argument marshalling only: every step of
+the hot path runs in libtgp.so's CUDA kernels.  There is no fallback: if the library is missing or
+a call fails, a TgpError is raised.
+
+Tensors passed to the device calls are torch CUDA tensors (PyTorch is used for device memory and
+streams only); parameters are exchanged as numpy float32 arrays on the host.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtgp.so")
+
+KIND = {"linear": 0, "resmlp": 1, "merge": 2, "batchnorm": 3}
+ACT = {"none": 0, "relu": 1, "gelu": 2}
+CKPT = {"always": 0, "except_last": 1, "never": 2}
+DTYPE = {"fp32": 0, "bf16": 1}
+# schedule record kinds (tgp_schedule)
+F, RECOMPUTE, B, COPY_F, COPY_B, SKIP_F, SKIP_B, W = range(8)
+
+
+class TgpError(RuntimeError):
+    pass
+
+
+class Layer(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("d_in", ctypes.c_int32), ("d_out", ctypes.c_int32),
+                ("d_hidden", ctypes.c_int32), ("act", ctypes.c_int32), ("dropout", ctypes.c_float),
+                ("stash_route", ctypes.c_int32), ("pop_route", ctypes.c_int32)]
+
+
+_lib = None
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+
+_SIGS = {
+    "tgp_balance": [ctypes.POINTER(ctypes.c_double), _I32, _I32, ctypes.POINTER(_I32)],
+    "tgp_split": [_I32, _I32, ctypes.POINTER(_I32)],
+    "tgp_schedule": [_I32, _I32, _I32, ctypes.POINTER(_I32), _I32, ctypes.POINTER(_I32), _I64,
+                     ctypes.POINTER(_I64)],
+    "tgp_create": [ctypes.POINTER(Layer), _I32, ctypes.POINTER(_I32), _I32, _I32, _I32, ctypes.POINTER(_I32),
+                   _I32, _I32, ctypes.c_uint64, ctypes.POINTER(_P)],
+    "tgp_destroy": [_P],
+    "tgp_ipc_export": [_P, _I32, _P, _I64, ctypes.POINTER(_I64)],
+    "tgp_ipc_import": [_P, _I32, _P, _I64],
+    "tgp_connect": [_P],
+    "tgp_forward": [_P, _P, _I32, _P],
+    "tgp_mse_loss_grad": [_P, _P, _P, _I32, _P, ctypes.POINTER(ctypes.c_double)],
+    "tgp_backward": [_P, _P, _P],
+    "tgp_step": [_P, ctypes.c_float],
+    "tgp_num_params": [_P, ctypes.POINTER(_I32)],
+    "tgp_param_info": [_P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I64)],
+    "tgp_set_param": [_P, _I32, _P],
+    "tgp_get_param": [_P, _I32, _P],
+    "tgp_get_grad": [_P, _I32, _P],
+    "tgp_init_params": [_P, ctypes.c_uint64],
+    "tgp_get_bn_running": [_P, _I32, _P, _P],
+    "tgp_get_issue_log": [_P, ctypes.POINTER(_I32), _I64, ctypes.POINTER(_I64)],
+    "tgp_set_trace": [_P, _I32],
+    "tgp_get_timeline": [_P, ctypes.POINTER(_I64), _I64, ctypes.POINTER(_I64)],
+    "tgp_kernel_count": [_P, ctypes.POINTER(_I64)],
+    "tgp_set_option": [_P, ctypes.c_char_p, _I64],
+    "tgp_last_error": [],
+    "tgp_bench_dominant_gemm": [_P, _I32, _I32, _I32, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)],
+    "tgp_test_gemm_bf16": [_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P],
+}
+
+
+def lib():
+    """Load libtgp.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise TgpError(f"{LIB_PATH} not found: build it with `python -m paper_2004_09910_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_char_p if name == "tgp_last_error" else (None if name == "tgp_destroy" else ctypes.c_int)
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return sorted(_SIGS)
+
+
+def _check(rc, what):
+    if rc != 0:
+        msg = lib().tgp_last_error()
+        raise TgpError(f"{what} failed ({rc}): {msg.decode() if msg else ''}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return ctypes.c_void_p(t.data_ptr())
+    return ctypes.c_void_p(int(t))
+
+
+def _ready(*tensors):
+    """The library works on its own non-blocking streams: make sure the work torch queued on the
+    caller's current stream for these tensors (their producers) has finished before handing them over."""
+    import torch
+
+    devs = {t.device for t in tensors if t is not None and hasattr(t, "device") and t.device.type == "cuda"}
+    for d in devs:
+        torch.cuda.current_stream(d).synchronize()
+
+
+# ------------------------------------------------------------------ pure host helpers
+def balance(costs, n):
+    c = (ctypes.c_double * len(costs))(*[float(v) for v in costs])
+    out = (_I32 * n)()
+    _check(lib().tgp_balance(c, len(costs), n, out), "tgp_balance")
+    return list(out)
+
+
+def split(B, m):
+    out = (_I32 * m)()
+    _check(lib().tgp_split(B, m, out), "tgp_split")
+    return list(out)
+
+
+def schedule(m, n, checkpoint="except_last", routes=()):
+    routes = list(routes)
+    r = (_I32 * max(1, 2 * len(routes)))(*[v for pr in routes for v in pr])
+    cnt = _I64()
+    _check(lib().tgp_schedule(m, n, CKPT[checkpoint], r, len(routes), None, 0, ctypes.byref(cnt)), "tgp_schedule")
+    buf = (_I32 * (8 * cnt.value))()
+    _check(lib().tgp_schedule(m, n, CKPT[checkpoint], r, len(routes), buf, cnt.value, ctypes.byref(cnt)),
+           "tgp_schedule")
+    return np.frombuffer(buf, dtype=np.int32).reshape(-1, 8).copy()
+
+
+def test_gemm_bf16(A, Bm, D, M, N, K, a_mn, b_mn, splits=0, stream=None):
+    _ready(A, Bm, D)
+    _check(lib().tgp_test_gemm_bf16(_ptr(A), _ptr(Bm), _ptr(D), M, N, K, int(a_mn), int(b_mn), splits,
+                                    _ptr(stream) if stream is not None else None), "tgp_test_gemm_bf16")
+
+
+def to_c_layers(layers):
+    arr = (Layer * len(layers))()
+    for q, L in enumerate(layers):
+        arr[q] = Layer(KIND[L["kind"]], L["d_in"], L["d_out"], L.get("d_hidden", 0), ACT[L.get("act", "none")],
+                       float(L.get("dropout", 0.0)), L.get("stash", -1), L.get("pop", -1))
+    return arr
+
+
+class Pipeline:
+    """A GPipe pipeline over this process's local partitions (tgp_ctx)."""
+
+    def __init__(self, layers, *, chunks, devices, balance=None, checkpoint="except_last", max_batch,
+                 dtype="bf16", seed=0):
+        self.layers = layers
+        self.n = len(devices)
+        self.m = chunks
+        self.devices = list(devices)
+        self._c_layers = to_c_layers(layers)
+        bal = None if balance is None else (_I32 * self.n)(*balance)
+        dev = (_I32 * self.n)(*devices)
+        h = _P()
+        _check(lib().tgp_create(self._c_layers, len(layers), bal, self.n, chunks, CKPT[checkpoint], dev, max_batch,
+                                DTYPE[dtype], seed, ctypes.byref(h)), "tgp_create")
+        self.h = h
+        n = _I32()
+        _check(lib().tgp_num_params(self.h, ctypes.byref(n)), "tgp_num_params")
+        self.n_params = n.value
+
+    def close(self):
+        if self.h:
+            lib().tgp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- multi-process wiring
+    def ipc_export(self, part):
+        n = _I64()
+        _check(lib().tgp_ipc_export(self.h, part, None, 0, ctypes.byref(n)), "tgp_ipc_export")
+        buf = ctypes.create_string_buffer(n.value)
+        _check(lib().tgp_ipc_export(self.h, part, buf, n.value, ctypes.byref(n)), "tgp_ipc_export")
+        return buf.raw
+
+    def ipc_import(self, part, blob):
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        _check(lib().tgp_ipc_import(self.h, part, buf, len(blob)), "tgp_ipc_import")
+
+    def connect(self):
+        _check(lib().tgp_connect(self.h), "tgp_connect")
+
+    # ---- training step
+    def forward(self, x, B, y):
+        _ready(x, y)
+        _check(lib().tgp_forward(self.h, _ptr(x), B, _ptr(y)), "tgp_forward")
+
+    def mse_loss_grad(self, y, t, B, dy):
+        loss = ctypes.c_double()
+        _ready(y, t, dy)
+        _check(lib().tgp_mse_loss_grad(self.h, _ptr(y), _ptr(t), B, _ptr(dy), ctypes.byref(loss)),
+               "tgp_mse_loss_grad")
+        return loss.value
+
+    def backward(self, dy, dx=None):
+        _ready(dy, dx)
+        _check(lib().tgp_backward(self.h, _ptr(dy), _ptr(dx)), "tgp_backward")
+
+    def step(self, lr):
+        _check(lib().tgp_step(self.h, ctypes.c_float(lr)), "tgp_step")
+
+    # ---- parameters
+    def param_info(self, idx):
+        layer, part, numel = _I32(), _I32(), _I64()
+        _check(lib().tgp_param_info(self.h, idx, ctypes.byref(layer), ctypes.byref(part), ctypes.byref(numel)),
+               "tgp_param_info")
+        return layer.value, part.value, numel.value
+
+    def set_param(self, idx, arr):
+        a = np.ascontiguousarray(arr, dtype=np.float32)
+        _check(lib().tgp_set_param(self.h, idx, a.ctypes.data_as(_P)), "tgp_set_param")
+
+    def get_param(self, idx, shape=None):
+        _, _, numel = self.param_info(idx)
+        a = np.empty(numel, dtype=np.float32)
+        _check(lib().tgp_get_param(self.h, idx, a.ctypes.data_as(_P)), "tgp_get_param")
+        return a.reshape(shape) if shape is not None else a
+
+    def get_grad(self, idx, shape=None):
+        _, _, numel = self.param_info(idx)
+        a = np.empty(numel, dtype=np.float32)
+        _check(lib().tgp_get_grad(self.h, idx, a.ctypes.data_as(_P)), "tgp_get_grad")
+        return a.reshape(shape) if shape is not None else a
+
+    def init_params(self, seed=0):
+        _check(lib().tgp_init_params(self.h, seed), "tgp_init_params")
+
+    def bn_running(self, layer, d):
+        mean = np.empty(d, np.float32)
+        var = np.empty(d, np.float32)
+        _check(lib().tgp_get_bn_running(self.h, layer, mean.ctypes.data_as(_P), var.ctypes.data_as(_P)),
+               "tgp_get_bn_running")
+        return mean, var
+
+    # ---- introspection
+    def issue_log(self):
+        n = _I64()
+        _check(lib().tgp_get_issue_log(self.h, None, 0, ctypes.byref(n)), "tgp_get_issue_log")
+        buf = (_I32 * (8 * max(1, n.value)))()
+        _check(lib().tgp_get_issue_log(self.h, buf, n.value, ctypes.byref(n)), "tgp_get_issue_log")
+        return np.frombuffer(buf, dtype=np.int32)[: 8 * n.value].reshape(-1, 8).copy()
+
+    def set_trace(self, on=True):
+        _check(lib().tgp_set_trace(self.h, int(on)), "tgp_set_trace")
+
+    def timeline(self):
+        n = _I64()
+        _check(lib().tgp_get_timeline(self.h, None, 0, ctypes.byref(n)), "tgp_get_timeline")
+        buf = (_I64 * (6 * max(1, n.value)))()
+        _check(lib().tgp_get_timeline(self.h, buf, n.value, ctypes.byref(n)), "tgp_get_timeline")
+        return np.frombuffer(buf, dtype=np.int64)[: 6 * n.value].reshape(-1, 6).copy()
+
+    def kernel_count(self):
+        n = _I64()
+        _check(lib().tgp_kernel_count(self.h, ctypes.byref(n)), "tgp_kernel_count")
+        return n.value
+
+    def bench_dominant_gemm(self, part, B, reps=3):
+        ms, by, n = ctypes.c_double(), ctypes.c_double(), _I64()
+        _check(lib().tgp_bench_dominant_gemm(self.h, part, B, reps, ctypes.byref(ms), ctypes.byref(by),
+                                             ctypes.byref(n)), "tgp_bench_dominant_gemm")
+        return ms.value, by.value, n.value
+
+    def set_option(self, name, value):
+        _check(lib().tgp_set_option(self.h, name.encode(), int(value)), "tgp_set_option")

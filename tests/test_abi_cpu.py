@@ -1,0 +1,107 @@
+"""CPU (no GPU) tests of the C-ABI library: it loads, exports every symbol include/tgp.h declares,
+and its pure host entry points (schedule emitter, balancer, split) agree bit-exactly with the
+oracle.  Argument validation of tgp_create happens before any CUDA call."""
+import ctypes
+import itertools
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2004_09910_b200 import tgp
+    if not os.path.exists(tgp.LIB_PATH):
+        from paper_2004_09910_b200.build import build
+        build(verbose=False)
+    return tgp
+
+
+def test_library_exports_every_header_symbol(L):
+    hdr = open(os.path.join(ROOT, "include", "tgp.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    declared = sorted(set(re.findall(r"\b(tgp_[a-z0-9_]+)\s*\(", hdr)))
+    assert len(declared) >= 25
+    lib = ctypes.CDLL(L.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    # the binding wraps exactly the declared functions
+    assert sorted(L.exported_symbols()) == declared
+
+
+def test_schedule_matches_oracle(L):
+    from oracle import schedule as S
+    for m, n, mode in itertools.product([1, 2, 3, 4, 8, 32], [1, 2, 3, 4, 8], S.MODES):
+        assert np.array_equal(L.schedule(m, n, mode), S.records(m, n, mode)), (m, n, mode)
+    for routes in ([(1, 7), (2, 6), (3, 5), (3, 4)], [(1, 4), (1, 4), (2, 2)], [(3, 3)]):
+        for m, mode in itertools.product([1, 4, 32], S.MODES):
+            got = L.schedule(m, 8, mode, routes)
+            assert np.array_equal(got, S.records(m, 8, mode, routes))
+
+
+def test_balance_matches_oracle(L):
+    from oracle import balance as B
+    rs = np.random.default_rng(11)
+    for trial in range(500):
+        Ln = int(rs.integers(1, 40))
+        n = int(rs.integers(1, min(8, Ln) + 1))
+        costs = [int(v) for v in rs.integers(0, 9, Ln)] if trial % 2 else [float(v) for v in rs.random(Ln)]
+        assert L.balance(costs, n) == B.balance_dp(costs, n)
+
+
+def test_split_matches_oracle(L):
+    from oracle import schedule as S
+    for B, m in [(8, 4), (10, 4), (512, 32), (7, 7), (100, 3), (1, 1)]:
+        assert L.split(B, m) == S.split_sizes(B, m)
+    with pytest.raises(L.TgpError):
+        L.split(3, 4)
+
+
+def test_create_validates_before_touching_cuda(L):
+    from synth import configs as C
+    bad = [
+        dict(chunks=0),                     # m < 1
+        dict(chunks=20, max_batch=16),      # m > B
+        dict(balance=[3, 2]),               # sum(balance) != n_layers
+        dict(balance=[4, 0]),               # empty partition
+    ]
+    for kw in bad:
+        args = dict(chunks=4, devices=[0, 0], balance=[2, 2], max_batch=16, dtype="fp32")
+        args.update(kw)
+        with pytest.raises(L.TgpError) as ei:
+            L.Pipeline(C.mlp_chain(4, 64), **args)
+        assert "(-1)" in str(ei.value)
+    # shape mismatch between consecutive layers
+    layers = C.mlp_chain(4, 64)
+    layers[2]["d_in"] = 32
+    with pytest.raises(L.TgpError):
+        L.Pipeline(layers, chunks=2, devices=[0], balance=[4], max_batch=4, dtype="fp32")
+    # pop before stash
+    layers = C.umlp(d=128, levels=1, blocks_per_level=1, mid_blocks=1)
+    layers[0]["stash"], layers[2]["pop"] = -1, 0
+    with pytest.raises(L.TgpError):
+        L.Pipeline(layers, chunks=2, devices=[0], balance=[len(layers)], max_batch=4, dtype="bf16")
+
+
+def test_no_cpu_fallback(L):
+    # a valid pipeline on a machine without a GPU must fail loudly (TGP_E_CUDA), never fall back
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from synth import configs as C
+    with pytest.raises(L.TgpError) as ei:
+        L.Pipeline(C.mlp_chain(4, 64), chunks=4, devices=[0, 0], balance=[2, 2], max_batch=16, dtype="fp32")
+    assert "(-3)" in str(ei.value) or "(-5)" in str(ei.value)
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2004_09910_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp", ".inc")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), f
