@@ -17,9 +17,9 @@ struct TcCfg {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int BUDGET = 196608;
   static constexpr int STAGES = (BUDGET / STAGE) > 12 ? 12 : (BUDGET / STAGE);
-  static constexpr int BNP = BN + 1;  // odd pitch: conflict-free partial-tile smem
-  static constexpr int RED_BYTES = 128 * BNP * 4;
-  static constexpr int DATA = (STAGES * STAGE > RED_BYTES) ? STAGES * STAGE : RED_BYTES;
+  static constexpr int RED_BYTES = 128 * BN * 4;           // fp32 partial tile (float4 quads)
+  static constexpr int CS_BYTES = (BN / 4) * 128 * 4;      // column-sum partials [quad][feature]
+  static constexpr int DATA = (STAGES * STAGE > RED_BYTES + CS_BYTES) ? STAGES * STAGE : RED_BYTES + CS_BYTES;
   static constexpr int SMEM = DATA + 1024 + 256;
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
@@ -176,43 +176,73 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     } else {
-      float* red = reinterpret_cast<float*>(smem);
+      // partial tile -> own smem as float4 quads: quad (chunk c, feature fl, q) at
+      // ((c*128 + fl)*4 + (q ^ (fl & 3))), the XOR spreading a warp's stores over the banks
+      float4* red4 = reinterpret_cast<float4*>(smem);
 #pragma unroll 1
       for (int c = 0; c < BN / 16; ++c) {
         float v[16];
         tmem_ld16(taddr + c * 16, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) red[fl * C::BNP + c * 16 + i] = nkb ? v[i] : 0.0f;
+        for (int q = 0; q < 4; ++q)
+          red4[(c * 128 + fl) * 4 + (q ^ (fl & 3))] =
+              nkb ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
   }
   tc_fence_before();
 
   if (p.epi.mode != EPI_DW) {
-    // ---------------- deterministic split-K reduction through DSMEM, fixed rank order
+    // ---------------- deterministic split-K reduction through DSMEM, fixed rank order.
+    // Rank r finalises features [r*128/S, (r+1)*128/S); work item = (feature, 4-row quad); all S
+    // remote quads are requested before the fixed-order sum.
     cluster_sync();
     const int S = gridDim.y;
     const int rank = (int)cluster_ctarank();
     const int rpr = 128 / S;
     const int et = (int)threadIdx.x - 64;
-    if (et >= 0 && et < rpr) {
-      const int fl = rank * rpr + et;
-      const int f = m0 + fl;
-      const int nvalid = min(BN, p.N - nb);
-      const uint32_t base = smem_u32(smem) + (uint32_t)(fl * C::BNP) * 4u;
-      uint32_t rb[8];
+    const int nvalid = min(BN, p.N - nb);
+    const int nq = (nvalid + 3) >> 2;
+    float* cs = reinterpret_cast<float*>(smem + C::RED_BYTES);  // [q][feature] column-sum partials
+    const bool want_cs = p.epi.mode == EPI_ACT_BWD && p.epi.colsum;
+    if (et >= 0) {
+      const uint32_t base = smem_u32(smem);
+      for (int it = et; it < rpr * nq; it += 128) {
+        const int fll = it % rpr, q = it / rpr;
+        const int fl = rank * rpr + fll;
+        const int f = m0 + fl;
+        const uint32_t off = (uint32_t)(((q >> 2) * 128 + fl) * 4 + ((q & 3) ^ (fl & 3))) * 16u;
+        float4 t[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) rb[q] = q < S ? mapa_shared(base, (uint32_t)q) : 0u;
-      float csum = 0.0f;
-#pragma unroll 1
-      for (int n = 0; n < nvalid; ++n) {
-        float acc = 0.0f;
+        for (int s = 0; s < 8; ++s)
+          if (s < S) t[s] = ld_dsmem_f32x4(mapa_shared(base + off, (uint32_t)s));
+        float4 a = t[0];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < S) acc += ld_dsmem_f32(rb[q] + 4u * (uint32_t)n);
-        if (f < p.M) csum += epi_apply(p.epi, f, nb + n, acc);
+        for (int s = 1; s < 8; ++s)
+          if (s < S) {
+            a.x += t[s].x;
+            a.y += t[s].y;
+            a.z += t[s].z;
+            a.w += t[s].w;
+          }
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        float part = 0.0f;
+        if (f < p.M) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * q + e < nvalid) part += epi_apply(p.epi, f, nb + 4 * q + e, av[e]);
+        }
+        if (want_cs) cs[q * rpr + fll] = part;
       }
-      if (p.epi.mode == EPI_ACT_BWD && p.epi.colsum && f < p.M) p.epi.colsum[f] = csum;
+      if (want_cs) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the 128 epilogue threads only
+        if (et < rpr) {
+          const int f = m0 + rank * rpr + et;
+          float s = 0.0f;
+          for (int q = 0; q < nq; ++q) s += cs[q * rpr + et];
+          if (f < p.M) p.epi.colsum[(int64_t)(nb / 16) * p.M + f] = s;
+        }
+      }
     }
     cluster_sync();
   }

@@ -40,6 +40,21 @@ int ln_fwd(cudaStream_t st, bool pdl, const float* x, int64_t ldx, int rows, int
 // per-micro-batch column partials dgamma_part = sum_rows dh n, dbeta_part = sum_rows dh.
 int ln_bwd(cudaStream_t st, bool pdl, const float* dh, const float* x, const float* mean, const float* rstd,
            const float* gamma, const float* dy, float* dx, int rows, int d, float* dgamma_part, float* dbeta_part);
+// Cluster LayerNorm (features split over a cluster, row statistics exchanged through DSMEM in fixed
+// rank order).  ln_fwd_cl falls back to ln_fwd for widths it cannot tile.  ln_bwd_cl writes the
+// column partials of 16-row block y to dgp/dbp + y*d (rowblocks >= ceil(rows/16); blocks past the
+// rows write zeros) and optionally `op` = dx in op dtype and `opsum` = its column partials.
+int ln_fwd_cl(cudaStream_t st, bool pdl, const float* x, int64_t ldx, int rows, int d, const float* gamma,
+              const float* beta, void* h, int64_t ldh, bool h_bf16, float* mean, float* rstd);
+int ln_bwd_cl(cudaStream_t st, bool pdl, const float* dh, const float* x, const float* mean, const float* rstd,
+              const float* gamma, const float* dy, float* dx, int rows, int d, int rowblocks, float* dgp, float* dbp,
+              void* op, bool op_bf16, float* opsum);
+bool ln_cluster_ok(int d);
+// out = op-dtype(src [* dropout(site, step)] * act'(z)), column partial sums per 16-row block into
+// colsum + y*d (nullable).  act = 0 and no dropout: a plain cast (+ partials).
+int colwise(cudaStream_t st, bool pdl, const float* src, int64_t lds, const float* z, int rows, int d, int act,
+            uint32_t drop_thresh, float drop_scale, uint64_t seed, const uint32_t* step, uint32_t site,
+            int64_t row_global0, void* out, int64_t ldo, bool out_bf16, float* colsum);
 // Convert rows x d fp32 to op dtype (optionally also column partial sums of the fp32 values).
 int convert_rows(cudaStream_t st, bool pdl, const float* x, int64_t ldx, int rows, int d, void* out, int64_t ldo,
                  bool out_bf16, float* colsum);

@@ -219,8 +219,8 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
     switch (L.L.kind) {
       case TGP_LINEAR:
       case TGP_MERGE: {
-        TGP_TRY(convert_rows(s.comp, pdl() && c->use_pdl, x, din, M, din, opptr(c, L.Xop, r0, din), din, c->bf16,
-                             nullptr));
+        TGP_TRY(colwise(s.comp, pdl() && c->use_pdl, x, din, nullptr, M, din, 0, 0u, 1.0f, c->seed, s.dstep,
+                        (uint32_t)l, r0, opptr(c, L.Xop, r0, din), din, c->bf16, nullptr));
         c->kernels++;
         e.mode = EPI_LINEAR_FWD;
         e.act = L.L.act;
@@ -250,7 +250,7 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
       }
       case TGP_RESMLP: {
         const int H = L.L.d_hidden;
-        TGP_TRY(ln_fwd(s.comp, pdl() && c->use_pdl, x, din, M, din, mparam(s, L, 0), mparam(s, L, 1),
+        TGP_TRY(ln_fwd_cl(s.comp, pdl() && c->use_pdl, x, din, M, din, mparam(s, L, 0), mparam(s, L, 1),
                        opptr(c, L.Hop, r0, din), din, c->bf16, L.mean[slot], L.rstd[slot]));
         c->kernels++;
         EpiParams e1 = e;
@@ -312,6 +312,7 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
     first_kernel = false;
     return r;
   };
+  bool dyop_ready = false;  // the next RESMLP's bf16 dY operand was already written by the LN backward above it
   for (int l = s.l1 - 1; l >= s.l0; --l) {
     LayerRT& L = c->layers[l];
     const int din = L.L.d_in, dout = L.L.d_out;
@@ -323,8 +324,10 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
       const float* ds = (R.dst == s.j) ? s.dskip_local[R.id] : s.self.dskip_in[R.id] + (size_t)r0 * R.width;
       TGP_TRY(add_rows(s.comp, pdl() && c->use_pdl, g, ds, (int64_t)M * dout));
       c->kernels++;
+      dyop_ready = false;
     }
-    const size_t po = (size_t)(i - 1);
+    const size_t po = (size_t)(i - 1) * c->pb;  // first 16-row partial block of micro-batch i
+    const size_t pbn = (size_t)(i - 1);          // BN per-micro-batch statistics
     EpiParams e{};
     e.op_bf16 = c->bf16 ? 1 : 0;
     e.seed = c->seed;
@@ -335,9 +338,9 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
       case TGP_LINEAR:
       case TGP_MERGE: {
         const float th_p = L.L.dropout;
-        TGP_TRY(act_bwd_rows(s.comp, pdl() && c->use_pdl, g, L.z[slot], M, dout, L.L.act, drop_thresh(th_p),
-                             th_p > 0 ? 1.0f / (1.0f - th_p) : 1.0f, c->seed, s.dstep, (uint32_t)l, r0,
-                             opptr(c, L.Zop, r0, dout), dout, c->bf16, L.pb + po * dout));
+        TGP_TRY(colwise(s.comp, pdl() && c->use_pdl, g, dout, L.z[slot], M, dout, L.L.act, drop_thresh(th_p),
+                        th_p > 0 ? 1.0f / (1.0f - th_p) : 1.0f, c->seed, s.dstep, (uint32_t)l, r0,
+                        opptr(c, L.Zop, r0, dout), dout, c->bf16, L.pb + po * dout));
         c->kernels++;
         const int K = din + L.d_skip;
         e.mode = EPI_STORE;
@@ -352,13 +355,16 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         // dx^T[m = in][n] = sum_k W[k = out][m] dZ[n][k]
         TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 0), dout, K, K}, true, Opnd{L.Zop, c->max_batch, dout, dout},
                          nullptr, false, K, M, dout, r0, dout, true, e));
+        dyop_ready = false;
         break;
       }
       case TGP_RESMLP: {
         const int H = L.L.d_hidden;
-        TGP_TRY(convert_rows(s.comp, pdl() && c->use_pdl, g, dout, M, dout, opptr(c, L.dYop, r0, dout), dout, c->bf16,
-                             L.pb2 + po * dout));
-        c->kernels++;
+        if (!dyop_ready) {
+          TGP_TRY(colwise(s.comp, pdl() && c->use_pdl, g, dout, nullptr, M, dout, 0, 0u, 1.0f, c->seed, s.dstep,
+                          (uint32_t)l, r0, opptr(c, L.dYop, r0, dout), dout, c->bf16, L.pb2 + po * dout));
+          c->kernels++;
+        }
         EpiParams e1 = e;
         e1.mode = EPI_ACT_BWD;
         e1.act = L.L.act;
@@ -381,16 +387,31 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         // dh^T[m = in][n] = sum_k W1[k = hidden][m] dA[n][k]
         TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 2), H, din, din}, true, Opnd{L.dAop, c->max_batch, H, H},
                          nullptr, false, din, M, H, r0, H, true, e2));
-        TGP_TRY(ln_bwd(s.comp, pdl() && c->use_pdl, s.dh, xin, L.mean[slot], L.rstd[slot], mparam(s, L, 0), g, dx, M,
-                       din, L.pg + po * din, L.pbt + po * din));
-        c->kernels += 2;
+        // the layer below consumes dx as its incoming gradient: if it is a RESMLP without a portal
+        // stash, emit its bf16 dY operand and b2 partial here (fused; no separate cast kernel)
+        LayerRT* below = (l > s.l0) ? &c->layers[l - 1] : nullptr;
+        const bool fuse = below && below->L.kind == TGP_RESMLP && below->L.stash_route < 0 && ln_cluster_ok(din);
+        if (ln_cluster_ok(din)) {
+          TGP_TRY(ln_bwd_cl(s.comp, pdl() && c->use_pdl, s.dh, xin, L.mean[slot], L.rstd[slot], mparam(s, L, 0), g, dx,
+                            M, din, c->pb, L.pg + po * din, L.pbt + po * din,
+                            fuse ? opptr(c, below->dYop, r0, din) : nullptr, c->bf16,
+                            fuse ? below->pb2 + po * din : nullptr));
+          c->kernels++;
+          dyop_ready = fuse;
+        } else {
+          TGP_TRY(ln_bwd(s.comp, pdl() && c->use_pdl, s.dh, xin, L.mean[slot], L.rstd[slot], mparam(s, L, 0), g, dx, M,
+                         din, L.pg + po * din, L.pbt + po * din));
+          c->kernels += 2;
+          dyop_ready = false;
+        }
         break;
       }
       case TGP_BATCHNORM: {
-        TGP_TRY(bn_bwd(s.comp, g, xin, L.z[slot], L.bn_mu + po * din, L.bn_rstd + po * din, mparam(s, L, 0), M, din,
+        TGP_TRY(bn_bwd(s.comp, g, xin, L.z[slot], L.bn_mu + pbn * din, L.bn_rstd + pbn * din, mparam(s, L, 0), M, din,
                        L.L.act, dx, L.pg + po * din, L.pb + po * din));
         c->kernels++;
         first_kernel = false;
+        dyop_ready = false;
         break;
       }
     }
@@ -424,7 +445,7 @@ static int exec_wgrad(tgp_ctx* c, Stage& s, int B) {
           TGP_TRY(run_gemm(c, s, false, Opnd{L.Zop, B, dout, dout}, true, Opnd{s.self.skip_in[R.id], B, R.width, R.width},
                            nullptr, true, dout, R.width, B, 0, B, false, e));
         }
-        TGP_TRY(reduce_partials(s.comp, L.pb, c->m, dout, gparam(s, L, 1), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pb, c->m * c->pb, dout, gparam(s, L, 1), acc));
         c->kernels++;
         break;
       }
@@ -438,16 +459,16 @@ static int exec_wgrad(tgp_ctx* c, Stage& s, int B) {
         e.ldw = H;
         TGP_TRY(run_gemm(c, s, false, Opnd{L.dYop, B, dout, dout}, true, Opnd{L.Gop, B, H, H}, nullptr, true, dout, H, B,
                          0, B, false, e));
-        TGP_TRY(reduce_partials(s.comp, L.pg, c->m, din, gparam(s, L, 0), acc));
-        TGP_TRY(reduce_partials(s.comp, L.pbt, c->m, din, gparam(s, L, 1), acc));
-        TGP_TRY(reduce_partials(s.comp, L.pb, c->m, H, gparam(s, L, 3), acc));
-        TGP_TRY(reduce_partials(s.comp, L.pb2, c->m, dout, gparam(s, L, 5), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pg, c->m * c->pb, din, gparam(s, L, 0), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pbt, c->m * c->pb, din, gparam(s, L, 1), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pb, c->m * c->pb, H, gparam(s, L, 3), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pb2, c->m * c->pb, dout, gparam(s, L, 5), acc));
         c->kernels += 4;
         break;
       }
       case TGP_BATCHNORM: {
-        TGP_TRY(reduce_partials(s.comp, L.pg, c->m, din, gparam(s, L, 0), acc));
-        TGP_TRY(reduce_partials(s.comp, L.pb, c->m, din, gparam(s, L, 1), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pg, c->m * c->pb, din, gparam(s, L, 0), acc));
+        TGP_TRY(reduce_partials(s.comp, L.pb, c->m * c->pb, din, gparam(s, L, 1), acc));
         c->kernels += 2;
         break;
       }

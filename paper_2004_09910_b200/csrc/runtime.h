@@ -83,6 +83,8 @@ struct Stage {
   __nv_bfloat16* shadow = nullptr;
   int64_t n_elems = 0;
   float* dh = nullptr;
+  float* partials = nullptr;  // all column-partial buffers of the partition (contiguous)
+  size_t partial_floats = 0;
   float* gbuf[2] = {nullptr, nullptr};
   uint32_t* counters = nullptr;  // [8]
   double* loss_buf = nullptr;
@@ -105,6 +107,7 @@ struct tgp_ctx {
   std::vector<tgp::Route> routes;
   std::vector<int> balance, devices, part_l0;
   int n = 0, m = 0, ckpt = 1, max_batch = 0, mb_cap = 0, nslots = 1;
+  int pb = 1;  // 16-row blocks per micro-batch: column-partial buffers are [m * pb][width]
   bool bf16 = false;
   uint64_t seed = 0;
   uint32_t step = 0;
