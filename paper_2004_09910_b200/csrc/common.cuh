@@ -159,6 +159,11 @@ TGP_DEV float4 ld_dsmem_f32x4(uint32_t addr) {
   return v;
 }
 
+TGP_DEV void st_dsmem_f32x4(uint32_t addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 TGP_DEV uint32_t elect_one() {
   uint32_t pred = 0;
   asm volatile(

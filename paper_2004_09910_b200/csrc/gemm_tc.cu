@@ -7,7 +7,26 @@
 #include "host.h"
 #include "kernels.h"
 
+#ifndef TGP_SKINNY_SMEM
+#define TGP_SKINNY_SMEM 92160
+#endif
+
 namespace tgp {
+
+#ifdef TGP_GEMM_TIMING
+// Debug instrumentation (variant builds only): per-CTA %globaltimer stamps of the last launches.
+__device__ unsigned long long g_ts[8192][5];
+__device__ unsigned int g_ts_next;
+TGP_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TGP_TS(slot) \
+  do { if (ts_row >= 0) g_ts[ts_row][slot] = gtimer(); } while (0)
+#else
+#define TGP_TS(slot) do {} while (0)
+#endif
 
 template <int BN>
 struct TcCfg {
@@ -15,12 +34,21 @@ struct TcCfg {
   static constexpr int A_BYTES = 128 * BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int BUDGET = 196608;
+  // Skinny (weight-streaming) tiles keep <= ~110 KB so two CTAs fit on an SM: with programmatic
+  // dependent launch the NEXT GEMM's CTA becomes resident and streams its weights while this one
+  // drains its epilogue.  Wide tiles (dW) take the whole SM.
+  static constexpr int BUDGET = BN <= 64 ? TGP_SKINNY_SMEM : 196608;
   static constexpr int STAGES = (BUDGET / STAGE) > 12 ? 12 : (BUDGET / STAGE);
   static constexpr int RED_BYTES = 128 * BN * 4;           // fp32 partial tile (float4 quads)
   static constexpr int CS_BYTES = (BN / 4) * 128 * 4;      // column-sum partials [quad][feature]
-  static constexpr int DATA = (STAGES * STAGE > RED_BYTES + CS_BYTES) ? STAGES * STAGE : RED_BYTES + CS_BYTES;
-  static constexpr int SMEM = DATA + 1024 + 256;
+  // skinny tiles reduce split-K by pushing partials into a dedicated receive region (one cluster
+  // barrier); wide tiles pull from the (aliased) stage buffers instead
+  static constexpr bool PUSH = BN <= 64;
+  static constexpr int RECV_BYTES = PUSH ? RED_BYTES : 0;
+  static constexpr int DATA = PUSH ? STAGES * STAGE
+                                   : ((STAGES * STAGE > RED_BYTES + CS_BYTES) ? STAGES * STAGE : RED_BYTES + CS_BYTES);
+  static constexpr int BAR_OFF = DATA + RECV_BYTES + (PUSH ? CS_BYTES : 0);
+  static constexpr int SMEM = BAR_OFF + 1024 + 256;
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
@@ -31,13 +59,20 @@ __global__ void __launch_bounds__(192, 1)
   using C = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tile = blockIdx.x, n_tile = blockIdx.z;
+#ifdef TGP_GEMM_TIMING
+  __shared__ int ts_row_s;
+  if (threadIdx.x == 0) ts_row_s = (int)(atomicAdd(&g_ts_next, 1u) % 8192u);
+  __syncthreads();
+  const int ts_row = ts_row_s;
+  if (threadIdx.x == 0) g_ts[ts_row][0] = gtimer();
+#endif
   const int nkb_total = p.K / C::BK;
   const int kb0 = blockIdx.y * p.kb_per_split;
   const int kb1 = min(kb0 + p.kb_per_split, nkb_total);
@@ -102,6 +137,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       griddep_wait();
+      TGP_TS(1);
       for (int it = 0; it < pre; ++it) load_b(it, kb0 + it);
       for (int it = pre; it < nkb; ++it) {
         const int s = it % C::STAGES, r = it / C::STAGES;
@@ -109,6 +145,18 @@ __global__ void __launch_bounds__(192, 1)
         mbar_arrive_expect_tx(&full[s], C::STAGE);
         load_a(s, kb0 + it);
         load_b(s, kb0 + it);
+      }
+      if (p.pf_bytes > 0) {
+        const int64_t ncta = (int64_t)gridDim.x * gridDim.y * gridDim.z;
+        const int64_t cid = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        const int64_t chunk = ((p.pf_bytes + ncta - 1) / ncta + 255) & ~int64_t(255);
+        const int64_t beg = cid * chunk;
+        const int64_t end = beg + chunk < p.pf_bytes ? beg + chunk : p.pf_bytes;
+        const char* base = reinterpret_cast<const char*>(p.pf_ptr);
+        for (int64_t o = beg; o < end; o += 65536) {
+          const uint32_t sz = (uint32_t)((end - o) < 65536 ? (end - o) : 65536);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"(sz) : "memory");
+        }
       }
     }
     // reconverge before the .aligned cluster barriers below (only one lane ran the producer loop)
@@ -133,6 +181,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         tc_commit(&empty[s]);
       }
+      TGP_TS(2);
       if (nkb > 0)
         tc_commit(tfull);
       else
@@ -144,6 +193,7 @@ __global__ void __launch_bounds__(192, 1)
     griddep_wait();
     mbar_wait(tfull, 0);
     tc_fence_after();
+    if (threadIdx.x == 64) TGP_TS(3);
     const int lg = warp & 3;  // TMEM lane group accessible to this warp
     const int fl = lg * 32 + lane;
     const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
@@ -175,6 +225,25 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
+    } else if (C::PUSH) {
+      // push: every rank STORES the slice of its partial tile owned by rank `owner` (features
+      // [owner*rpr, +rpr)) into the owner's dedicated receive region, slot = source rank:
+      // quad (src, c, fll, q) at float4 ((src*(BN/16) + c)*rpr + fll)*4 + (q ^ (fll & 3)).
+      const int S = gridDim.y, rpr = 128 / S;
+      const int owner = fl / rpr, fll = fl % rpr, src = (int)cluster_ctarank();
+      const uint32_t recv = smem_u32(smem + C::DATA);
+#pragma unroll 1
+      for (int c = 0; c < BN / 16; ++c) {
+        float v[16];
+        tmem_ld16(taddr + c * 16, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t idx = (uint32_t)(((src * (BN / 16) + c) * rpr + fll) * 4 + (q ^ (fll & 3)));
+          const float4 val =
+              nkb ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+          st_dsmem_f32x4(mapa_shared(recv + idx * 16u, (uint32_t)owner), val);
+        }
+      }
     } else {
       // partial tile -> own smem as float4 quads: quad (chunk c, feature fl, q) at
       // ((c*128 + fl)*4 + (q ^ (fl & 3))), the XOR spreading a warp's stores over the banks
@@ -192,7 +261,50 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
 
-  if (p.epi.mode != EPI_DW) {
+  if (p.epi.mode != EPI_DW && C::PUSH) {
+    // ---------------- one cluster barrier, then a purely local fixed-order (source-rank) sum
+    cluster_sync();
+    const int S = gridDim.y;
+    const int rank = (int)cluster_ctarank();
+    const int rpr = 128 / S;
+    const int et = (int)threadIdx.x - 64;
+    const int nvalid = min(BN, p.N - nb);
+    const int nq = (nvalid + 3) >> 2;
+    const float4* recv4 = reinterpret_cast<const float4*>(smem + C::DATA);
+    float* cs = reinterpret_cast<float*>(smem + C::DATA + C::RECV_BYTES);
+    const bool want_cs = p.epi.mode == EPI_ACT_BWD && p.epi.colsum;
+    if (et >= 0) {
+      for (int it = et; it < rpr * nq; it += 128) {
+        const int fll = it % rpr, q = it / rpr;
+        const int f = m0 + rank * rpr + fll;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s = 0; s < S; ++s) {
+          const float4 t = recv4[((s * (BN / 16) + (q >> 2)) * rpr + fll) * 4 + ((q & 3) ^ (fll & 3))];
+          a.x += t.x;
+          a.y += t.y;
+          a.z += t.z;
+          a.w += t.w;
+        }
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        float part = 0.0f;
+        if (f < p.M) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * q + e < nvalid) part += epi_apply(p.epi, f, nb + 4 * q + e, av[e]);
+        }
+        if (want_cs) cs[q * rpr + fll] = part;
+      }
+      if (want_cs) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the 128 epilogue threads only
+        if (et < rpr) {
+          const int f = m0 + rank * rpr + et;
+          float s = 0.0f;
+          for (int q = 0; q < nq; ++q) s += cs[q * rpr + et];
+          if (f < p.M) p.epi.colsum[(int64_t)(nb / 16) * p.M + f] = s;
+        }
+      }
+    }
+  } else if (p.epi.mode != EPI_DW) {
     // ---------------- deterministic split-K reduction through DSMEM, fixed rank order.
     // Rank r finalises features [r*128/S, (r+1)*128/S); work item = (feature, 4-row quad); all S
     // remote quads are requested before the fixed-order sum.
@@ -248,6 +360,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (threadIdx.x == 0) TGP_TS(4);
 }
 
 // ---------------------------------------------------------------------------------- host side
@@ -336,6 +449,8 @@ int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B
     const int mt = p.M / 128;
     S = splits > 0 ? splits : env_int("TGP_SPLITK", 0);
     if (S <= 0) {
+      // ~one wave of 148 CTAs (measured: in the full step, split 4 beats split 8 at C2 although an
+      // isolated PDL-chained GEMM prefers 8 -- profiles/gemm_timeline.py)
       S = (148 + mt * ntiles / 2) / (mt * ntiles);
     }
     S = std::max(1, std::min(S, 8));
@@ -378,3 +493,17 @@ int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B
 }
 
 }  // namespace tgp
+
+#ifdef TGP_GEMM_TIMING
+extern "C" int tgp_debug_timestamps(unsigned long long* out, int cap, int reset) {
+  unsigned int n = 0;
+  cudaMemcpyFromSymbol(&n, tgp::g_ts_next, 4);
+  const int m = (int)(n < (unsigned)cap ? n : (unsigned)cap);
+  cudaMemcpyFromSymbol(out, tgp::g_ts, (size_t)m * 5 * 8);
+  if (reset) {
+    unsigned int z = 0;
+    cudaMemcpyToSymbol(tgp::g_ts_next, &z, 4);
+  }
+  return m;
+}
+#endif

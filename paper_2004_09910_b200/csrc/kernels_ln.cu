@@ -38,11 +38,19 @@ __device__ __forceinline__ float rowset_total(int row, float (*sh)[4]) {
   return s;
 }
 
-// exchange: each CTA publishes xp[16]; every thread reads the CL values of its row in rank order
-__device__ __forceinline__ float cluster_row_sum(const float* xp_local, int row, int CL) {
-  const uint32_t a = smem_u32(xp_local + row);
+// Cluster exchange of per-row partials: every CTA publishes xp[nv][16]; one parallel gather pulls
+// the CL ranks' values into local smem (one remote load per thread), then each row total is a
+// local sum over the ranks in FIXED rank order (bit-identical on every CTA of the cluster).
+__device__ __forceinline__ void cluster_gather(const float* xp, int nv, float* gath, int CL) {
+  for (int t = threadIdx.x; t < nv * 16 * CL; t += blockDim.x) {
+    const int v = t / (16 * CL), q = (t / 16) % CL, row = t % 16;
+    gath[(v * 16 + q) * 16 + row] = ld_dsmem_f32(mapa_shared(smem_u32(xp + v * 16 + row), (uint32_t)q));
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ float gathered_total(const float* gath, int v, int row, int CL) {
   float s = 0.0f;
-  for (int q = 0; q < CL; ++q) s += ld_dsmem_f32(mapa_shared(a, (uint32_t)q));
+  for (int q = 0; q < CL; ++q) s += gath[(v * 16 + q) * 16 + row];
   return s;
 }
 
@@ -55,6 +63,7 @@ __global__ void __launch_bounds__(256) ln_fwd_cl_kernel(const float* __restrict_
   constexpr int RS = 256 / NQ, RPT = 16 / RS;
   __shared__ float sh[16][4];
   __shared__ float xp[2][16];
+  __shared__ float gath[2 * 16 * 16];
   griddep_wait();
   griddep_launch();
   const int CL = gridDim.x;
@@ -73,11 +82,11 @@ __global__ void __launch_bounds__(256) ln_fwd_cl_kernel(const float* __restrict_
   __syncthreads();
   if (threadIdx.x < 16) xp[0][threadIdx.x] = rowset_total<NQ>(threadIdx.x, sh);
   cluster_sync();
+  cluster_gather(&xp[0][0], 1, gath, CL);
   float mu[RPT];
 #pragma unroll
-  for (int k = 0; k < RPT; ++k) mu[k] = cluster_row_sum(xp[0], rs + k * RS, CL) / (float)d;
+  for (int k = 0; k < RPT; ++k) mu[k] = gathered_total(gath, 0, rs + k * RS, CL) / (float)d;
   // pass 2: centred second moment
-  __syncthreads();
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
     const float a = v[k].x - mu[k], b = v[k].y - mu[k], e = v[k].z - mu[k], f = v[k].w - mu[k];
@@ -86,12 +95,13 @@ __global__ void __launch_bounds__(256) ln_fwd_cl_kernel(const float* __restrict_
   __syncthreads();
   if (threadIdx.x < 16) xp[1][threadIdx.x] = rowset_total<NQ>(threadIdx.x, sh);
   cluster_sync();
+  cluster_gather(&xp[1][0], 1, gath + 256, CL);
   const float4 g = *reinterpret_cast<const float4*>(gamma + c0);
   const float4 bb = *reinterpret_cast<const float4*>(beta + c0);
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
     const int rl = rs + k * RS, r = rb0 + rl;
-    const float var = cluster_row_sum(xp[1], rl, CL) / (float)d;
+    const float var = gathered_total(gath + 256, 0, rl, CL) / (float)d;
     const float rsd = 1.0f / sqrtf(var + 1e-5f);
     if (r < rows) {
       const float o0 = g.x * ((v[k].x - mu[k]) * rsd) + bb.x, o1 = g.y * ((v[k].y - mu[k]) * rsd) + bb.y;
@@ -129,6 +139,7 @@ __global__ void __launch_bounds__(256) ln_bwd_cl_kernel(const float* __restrict_
   __shared__ float sh[16][4];
   __shared__ float xp[2][16];
   __shared__ float4 cp[3][RS][NQ];
+  __shared__ float gath[2 * 16 * 16];
   griddep_wait();
   griddep_launch();
   const int CL = gridDim.x;
@@ -170,12 +181,13 @@ __global__ void __launch_bounds__(256) ln_bwd_cl_kernel(const float* __restrict_
   __syncthreads();
   if (threadIdx.x < 16) xp[1][threadIdx.x] = rowset_total<NQ>(threadIdx.x, sh);
   cluster_sync();
+  cluster_gather(&xp[0][0], 2, gath, CL);
   float4 sg = make_float4(0.f, 0.f, 0.f, 0.f), sb = sg, so = sg;
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
     const int rl = rs + k * RS, r = rb0 + rl;
-    const float m1 = cluster_row_sum(xp[0], rl, CL) / (float)d;
-    const float m2 = cluster_row_sum(xp[1], rl, CL) / (float)d;
+    const float m1 = gathered_total(gath, 0, rl, CL) / (float)d;
+    const float m2 = gathered_total(gath, 1, rl, CL) / (float)d;
     if (r < rows) {
       const float4 dyv = *reinterpret_cast<const float4*>(dy + (int64_t)r * d + c0);
       const float4 n = vn[k], a = vdh[k];

@@ -148,9 +148,16 @@ struct Opnd {
 }  // namespace
 
 // D[m][n] = sum_k A(m,k) B(n,k);  a_mn: A memory [K][M], else [M][K];  b_mn: B memory [K][N] else [rows][K]
+struct Prefetch {
+  const void* p = nullptr;
+  int64_t bytes = 0;
+};
+
 static int run_gemm(tgp_ctx* c, Stage& s, bool pdl, Opnd A, bool a_mn, Opnd B0, const Opnd* B1, bool b_mn, int M,
-                    int N, int K, int n0, int k_seg, bool a_weight, const EpiParams& e) {
+                    int N, int K, int n0, int k_seg, bool a_weight, const EpiParams& e, Prefetch pf = Prefetch{}) {
   GemmParams p{};
+  p.pf_ptr = c->prefetch ? pf.p : nullptr;
+  p.pf_bytes = c->prefetch ? (pf.bytes & ~int64_t(15)) : 0;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -193,6 +200,27 @@ static void* stash_dst(tgp_ctx* c, Stage& s, int r, int64_t r0) {
   const Route& R = c->routes[r];
   void* base = (R.dst == s.j) ? s.self.skip_in[r] : s.skip_send[r];
   return opptr(c, base, r0, R.width);
+}
+
+// The first weight matrix a layer's forward / backward GEMM sequence streams (for the L2 prefetch
+// issued by the GEMM before it; the sequence of GEMMs inside a task is static).
+static Prefetch first_fwd_weight(tgp_ctx* c, Stage& s, const LayerRT& L) {
+  if (!c->bf16) return Prefetch{};
+  if (L.L.kind == TGP_RESMLP) return Prefetch{wparam(c, s, L, 2), L.pnum[2] * 2};
+  if (L.L.kind == TGP_LINEAR || L.L.kind == TGP_MERGE) return Prefetch{wparam(c, s, L, 0), L.pnum[0] * 2};
+  return Prefetch{};
+}
+static Prefetch first_bwd_weight(tgp_ctx* c, Stage& s, const LayerRT& L) {
+  if (!c->bf16) return Prefetch{};
+  if (L.L.kind == TGP_RESMLP) return Prefetch{wparam(c, s, L, 4), L.pnum[4] * 2};
+  if (L.L.kind == TGP_LINEAR || L.L.kind == TGP_MERGE) return Prefetch{wparam(c, s, L, 0), L.pnum[0] * 2};
+  return Prefetch{};
+}
+static Prefetch next_fwd(tgp_ctx* c, Stage& s, int l) {  // after the last GEMM of layer l (forward order)
+  return first_fwd_weight(c, s, c->layers[l + 1 < s.l1 ? l + 1 : s.l0]);
+}
+static Prefetch next_bwd(tgp_ctx* c, Stage& s, int l) {  // after the last GEMM of layer l (backward order)
+  return first_bwd_weight(c, s, c->layers[l - 1 >= s.l0 ? l - 1 : s.l1 - 1]);
 }
 
 // ============================================================================ task executors
@@ -242,9 +270,9 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         if (L.L.kind == TGP_MERGE) {
           const Route& R = c->routes[L.L.pop_route];
           Opnd B1{s.self.skip_in[R.id], c->max_batch, R.width, R.width};
-          TGP_TRY(run_gemm(c, s, pdl(), A, false, B0, &B1, false, dout, M, K, r0, din, true, e));
+          TGP_TRY(run_gemm(c, s, pdl(), A, false, B0, &B1, false, dout, M, K, r0, din, true, e, next_fwd(c, s, l)));
         } else {
-          TGP_TRY(run_gemm(c, s, pdl(), A, false, B0, nullptr, false, dout, M, K, r0, K, true, e));
+          TGP_TRY(run_gemm(c, s, pdl(), A, false, B0, nullptr, false, dout, M, K, r0, K, true, e, next_fwd(c, s, l)));
         }
         break;
       }
@@ -265,7 +293,8 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         e1.drop_scale = L.L.dropout > 0 ? 1.0f / (1.0f - L.L.dropout) : 1.0f;
         e1.drop_width = H;
         TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 2), H, din, din}, false,
-                         Opnd{L.Hop, c->max_batch, din, din}, nullptr, false, H, M, din, r0, din, true, e1));
+                         Opnd{L.Hop, c->max_batch, din, din}, nullptr, false, H, M, din, r0, din, true, e1,
+                         Prefetch{wparam(c, s, L, 4), L.pnum[4] * 2}));
         EpiParams e2 = e;
         e2.mode = EPI_RESID_FWD;
         e2.bias = mparam(s, L, 5);
@@ -278,7 +307,7 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
           e2.ld_op = dout;
         }
         TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 4), dout, H, H}, false, Opnd{L.Gop, c->max_batch, H, H},
-                         nullptr, false, dout, M, H, r0, H, true, e2));
+                         nullptr, false, dout, M, H, r0, H, true, e2, next_fwd(c, s, l)));
         break;
       }
       case TGP_BATCHNORM: {
@@ -354,7 +383,7 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         }
         // dx^T[m = in][n] = sum_k W[k = out][m] dZ[n][k]
         TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 0), dout, K, K}, true, Opnd{L.Zop, c->max_batch, dout, dout},
-                         nullptr, false, K, M, dout, r0, dout, true, e));
+                         nullptr, false, K, M, dout, r0, dout, true, e, next_bwd(c, s, l)));
         dyop_ready = false;
         break;
       }
@@ -378,7 +407,7 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         e1.drop_width = H;
         // dg^T[m = hidden][n] = sum_k W2[k = out][m] dY[n][k]
         TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 4), dout, H, H}, true, Opnd{L.dYop, c->max_batch, dout, dout},
-                         nullptr, false, H, M, dout, r0, dout, true, e1));
+                         nullptr, false, H, M, dout, r0, dout, true, e1, Prefetch{wparam(c, s, L, 2), L.pnum[2] * 2}));
         EpiParams e2 = e;
         e2.mode = EPI_STORE;
         e2.out0 = s.dh;
@@ -386,7 +415,7 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         e2.split_f = din;
         // dh^T[m = in][n] = sum_k W1[k = hidden][m] dA[n][k]
         TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 2), H, din, din}, true, Opnd{L.dAop, c->max_batch, H, H},
-                         nullptr, false, din, M, H, r0, H, true, e2));
+                         nullptr, false, din, M, H, r0, H, true, e2, next_bwd(c, s, l)));
         // the layer below consumes dx as its incoming gradient: if it is a RESMLP without a portal
         // stash, emit its bf16 dY operand and b2 partial here (fused; no separate cast kernel)
         LayerRT* below = (l > s.l0) ? &c->layers[l - 1] : nullptr;

@@ -123,7 +123,7 @@ struct tgp_ctx {
   std::vector<int> slot_of;  // 1-based micro-batch -> slot
   int64_t kernels = 0;
   // options
-  bool use_graphs = true, use_pdl = true, trace = false, poison = false;
+  bool use_graphs = true, use_pdl = true, trace = false, poison = false, prefetch = false;
   int splitk = 0, skip_wait_part = -1;
   bool can_flush = false;
   std::vector<tgp::TraceRec> trace_recs;

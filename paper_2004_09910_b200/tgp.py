@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtgp.so")
+LIB_PATH = os.environ.get("TGP_LIB") or os.path.join(_HERE, "libtgp.so")
 
 KIND = {"linear": 0, "resmlp": 1, "merge": 2, "batchnorm": 3}
 ACT = {"none": 0, "relu": 1, "gelu": 2}
