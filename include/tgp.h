@@ -170,10 +170,15 @@ tgp_status tgp_get_timeline(tgp_ctx* ctx, int64_t* rec, int64_t cap, int64_t* n_
 /* Number of kernels this process launched (or replayed through CUDA graphs) since creation. */
 tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
 
-/* Runtime options: "graphs" (1 = capture each task's kernels into a CUDA graph; default 1),
- * "pdl" (programmatic dependent launch between a task's kernels; default 1),
- * "splitk" (0 = auto), "test_poison" (fill receive slots with NaN before each call, for the
- * negative-control tests), "test_skip_wait" (drop the receive wait of partition `value`). */
+/* Runtime options (TGP_E_INVALID for an unknown name):
+ *  "graphs"   1 = capture each task's kernels into a CUDA graph and replay it (default 1)
+ *  "pdl"      programmatic dependent launch between the kernels of a task (default 1)
+ *  "splitk"   split-K cluster size of the weight-streaming GEMMs, 0 = automatic (default 0)
+ *  "prefetch" L2 prefetch of the next GEMM's weights by the previous GEMM (default 0)
+ * Test-only negative controls (never used on the product path):
+ *  "test_poison"        fill the forward receive slabs with NaN before each forward call
+ *  "test_skip_wait"     drop the receive waits of partition `value` (-1 = none)
+ *  "test_delay_push_us" delay every push on its copy stream by `value` microseconds */
 tgp_status tgp_set_option(tgp_ctx* ctx, const char* name, int64_t value);
 
 const char* tgp_last_error(void);

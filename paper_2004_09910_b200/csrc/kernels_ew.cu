@@ -469,6 +469,16 @@ int push_bytes(cudaStream_t st, const void* src, void* dst, int64_t nbytes, uint
                 (const int4*)src, (int4*)dst, nbytes / 16, counter, flag, seq);
 }
 
+// test-only: occupy a stream for `ns` nanoseconds (negative-control tests delay a push with it)
+__global__ void spin_kernel(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+int spin(cudaStream_t st, uint64_t ns) { return launch("spin", spin_kernel, dim3(1), dim3(1), st, false, ns); }
+
 __global__ void signal_kernel(uint32_t* flag, uint32_t v) {
   __threadfence_system();
   st_release_sys(flag, v);

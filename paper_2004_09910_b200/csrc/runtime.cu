@@ -619,6 +619,10 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
         first_push[src][dst] = 1;
       }
       const ArenaView& pv = c->view[dst];
+      if (c->delay_push_ns) {  // negative-control tests: make a missing receive wait observable
+        TGP_TRY(spin(st, c->delay_push_ns));
+        c->kernels++;
+      }
       cudaEvent_t ta = nullptr;
       trace_begin(c, s, st, skip ? 2 : 1, rc.kind, i, &ta);
       uint32_t* ctr = s.counters + (skip ? 1 : 0);

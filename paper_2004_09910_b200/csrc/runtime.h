@@ -125,6 +125,7 @@ struct tgp_ctx {
   // options
   bool use_graphs = true, use_pdl = true, trace = false, poison = false, prefetch = false;
   int splitk = 0, skip_wait_part = -1;
+  uint64_t delay_push_ns = 0;
   bool can_flush = false;
   std::vector<tgp::TraceRec> trace_recs;
   std::vector<int64_t> timeline;
