@@ -175,6 +175,8 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *  "pdl"      programmatic dependent launch between the kernels of a task (default 1)
  *  "splitk"   split-K cluster size of the weight-streaming GEMMs, 0 = automatic (default 0)
  *  "prefetch" L2 prefetch of the next GEMM's weights by the previous GEMM (default 0)
+ *  "persistent" run F / F' of all-RESMLP partitions (<= 16-row micro-batches) as ONE cooperative
+ *             persistent kernel with grid barriers between phases (default 0)
  * Test-only negative controls (never used on the product path):
  *  "test_poison"        fill the forward receive slabs with NaN before each forward call
  *  "test_skip_wait"     drop the receive waits of partition `value` (-1 = none)
@@ -191,6 +193,11 @@ const char* tgp_last_error(void);
  * activation operand + epilogue reads/writes); *launches: launches timed. */
 tgp_status tgp_bench_dominant_gemm(tgp_ctx* ctx, int32_t part, int32_t B, int32_t reps, double* ms, double* bytes,
                                    int64_t* launches);
+
+/* Diagnostics of the persistent forward-task kernel (only when the process runs with TGP_PT_DEBUG
+ * set): per CTA and grid-barrier id k < 256, the %globaltimer at its arrival and release, as
+ * [grid][256][2] uint64.  out may be NULL to query *n. */
+tgp_status tgp_debug_pt_read(tgp_ctx* ctx, int32_t part, uint64_t* out, int64_t cap, int64_t* n);
 
 /* ------------------------------------------------------------------ kernel-level test entry */
 

@@ -43,6 +43,16 @@ TGP_DEV bool mbar_try_wait(uint32_t bar, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
+// Non-blocking probe (try_wait may suspend the thread for a hardware time limit).
+TGP_DEV bool mbar_test_wait(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
 TGP_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t a = smem_u32(bar);
   while (!mbar_try_wait(a, phase)) {

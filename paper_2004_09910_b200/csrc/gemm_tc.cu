@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ---------------------------------------------------------------------------------- host side
-static bool make_map(CUtensorMap* map, const TcMat& t, int box_inner, int box_outer) {
+bool make_map(CUtensorMap* map, const TcMat& t, int box_inner, int box_outer) {
   const Driver* d = driver();
   if (!d) return false;
   cuuint64_t dims[2] = {(cuuint64_t)t.cols, (cuuint64_t)t.rows};
