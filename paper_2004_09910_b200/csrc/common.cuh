@@ -169,6 +169,15 @@ TGP_DEV float4 ld_dsmem_f32x4(uint32_t addr) {
   return v;
 }
 
+// Asynchronous store into another CTA's shared memory that completes bytes on THAT CTA's mbarrier
+// (both addresses mapped with mapa to the same destination CTA).
+TGP_DEV void st_async_f32x4(uint32_t addr, float4 v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(addr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(mbar)
+               : "memory");
+}
+TGP_DEV void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+TGP_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 TGP_DEV void st_dsmem_f32x4(uint32_t addr, float4 v) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");

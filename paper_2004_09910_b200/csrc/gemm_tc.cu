@@ -15,7 +15,7 @@ namespace tgp {
 
 #ifdef TGP_GEMM_TIMING
 // Debug instrumentation (variant builds only): per-CTA %globaltimer stamps of the last launches.
-__device__ unsigned long long g_ts[8192][5];
+__device__ unsigned long long g_ts[8192][8];
 __device__ unsigned int g_ts_next;
 TGP_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* rbar = tfull + 1;  // split-K receive region complete (PUSH tiles)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tile = blockIdx.x, n_tile = blockIdx.z;
@@ -87,6 +88,12 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
+    if (C::PUSH && p.epi.mode != EPI_DW) {
+      // every byte of the receive region is written once by the S cluster ranks' st.async
+      mbar_init(rbar, 1);
+      fence_barrier_init();
+      mbar_arrive_expect_tx(rbar, (uint32_t)C::RED_BYTES);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -95,6 +102,10 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   griddep_launch();
+  // receive barriers of all cluster ranks must be initialised before anyone pushes into them:
+  // arrive now, wait right before the first push (the whole mainloop in between)
+  const bool push_red = C::PUSH && p.epi.mode != EPI_DW;
+  if (push_red) cluster_arrive();
 
   auto stage_a = [&](int s) { return smem + s * C::STAGE; };
   auto stage_b = [&](int s) { return smem + s * C::STAGE + C::A_BYTES; };
@@ -161,6 +172,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     // reconverge before the .aligned cluster barriers below (only one lane ran the producer loop)
     __syncwarp();
+    if (push_red) cluster_wait();
   } else if (warp == 1) {
     if (elect_one()) {
       // ---------------- MMA issuer (single thread)
@@ -188,6 +200,7 @@ __global__ void __launch_bounds__(192, 1)
         mbar_arrive(tfull);
     }
     __syncwarp();
+    if (push_red) cluster_wait();
   } else {
     // ---------------- epilogue warps 2..5: TMEM -> registers
     griddep_wait();
@@ -232,6 +245,8 @@ __global__ void __launch_bounds__(192, 1)
       const int S = gridDim.y, rpr = 128 / S;
       const int owner = fl / rpr, fll = fl % rpr, src = (int)cluster_ctarank();
       const uint32_t recv = smem_u32(smem + C::DATA);
+      const uint32_t rmbar = mapa_shared(smem_u32(rbar), (uint32_t)owner);
+      cluster_wait();  // every rank's receive barrier is initialised (arrived right after setup)
 #pragma unroll 1
       for (int c = 0; c < BN / 16; ++c) {
         float v[16];
@@ -241,9 +256,11 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t idx = (uint32_t)(((src * (BN / 16) + c) * rpr + fll) * 4 + (q ^ (fll & 3)));
           const float4 val =
               nkb ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
-          st_dsmem_f32x4(mapa_shared(recv + idx * 16u, (uint32_t)owner), val);
+          // completes 16 bytes on the OWNER's receive barrier: no cluster-wide barrier afterwards
+          st_async_f32x4(mapa_shared(recv + idx * 16u, (uint32_t)owner), val, rmbar);
         }
       }
+      if (threadIdx.x == 64) TGP_TS(5);
     } else {
       // partial tile -> own smem as float4 quads: quad (chunk c, feature fl, q) at
       // ((c*128 + fl)*4 + (q ^ (fl & 3))), the XOR spreading a warp's stores over the banks
@@ -262,8 +279,10 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
 
   if (p.epi.mode != EPI_DW && C::PUSH) {
-    // ---------------- one cluster barrier, then a purely local fixed-order (source-rank) sum
-    cluster_sync();
+    // ---------------- wait for the S ranks' partials (local mbarrier), then a purely local
+    // fixed-order (source-rank) sum
+    if (threadIdx.x >= 64) mbar_wait(rbar, 0);
+    if (threadIdx.x == 64) TGP_TS(6);
     const int S = gridDim.y;
     const int rank = (int)cluster_ctarank();
     const int rpr = 128 / S;
@@ -304,6 +323,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
+    if (threadIdx.x == 64) TGP_TS(7);
   } else if (p.epi.mode != EPI_DW) {
     // ---------------- deterministic split-K reduction through DSMEM, fixed rank order.
     // Rank r finalises features [r*128/S, (r+1)*128/S); work item = (feature, 4-row quad); all S
@@ -499,7 +519,7 @@ extern "C" int tgp_debug_timestamps(unsigned long long* out, int cap, int reset)
   unsigned int n = 0;
   cudaMemcpyFromSymbol(&n, tgp::g_ts_next, 4);
   const int m = (int)(n < (unsigned)cap ? n : (unsigned)cap);
-  cudaMemcpyFromSymbol(out, tgp::g_ts, (size_t)m * 5 * 8);
+  cudaMemcpyFromSymbol(out, tgp::g_ts, (size_t)m * 8 * 8);
   if (reset) {
     unsigned int z = 0;
     cudaMemcpyToSymbol(tgp::g_ts_next, &z, 4);

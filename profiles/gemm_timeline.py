@@ -24,7 +24,7 @@ f = lib.tgp_debug_timestamps
 f.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
 f.restype = ctypes.c_int
 P.bench_dominant_gemm(0, 512, reps=1)  # warm
-buf = np.zeros((8192, 5), dtype=np.uint64)
+buf = np.zeros((8192, 8), dtype=np.uint64)
 f(buf.ctypes.data, 8192, 1)
 ms, by, n = P.bench_dominant_gemm(0, 512, reps=1)
 cnt = f(buf.ctypes.data, 8192, 1)
@@ -39,9 +39,14 @@ for k in range(launches):
     r = rows[k * ncta:(k + 1) * ncta] - t0
     st, wt, mm, tf, en = r[:, 0], r[:, 1], r[:, 2], r[:, 3], r[:, 4]
     wt = wt[wt > -t0 // 2]
+    raw = rows[k * ncta:(k + 1) * ncta]
+    pu, rv, cs = (raw[:, c][raw[:, c] > 0] - t0 for c in (5, 6, 7))
     line = (f"L{k:02d} start[min {st.min() / 1e3:8.2f} max {st.max() / 1e3:8.2f}] "
             f"wait_done[min {wt.min() / 1e3:8.2f} max {wt.max() / 1e3:8.2f}] mma_done max {mm.max() / 1e3:8.2f} "
             f"epi_start max {tf.max() / 1e3:8.2f} exit[min {en.min() / 1e3:8.2f} max {en.max() / 1e3:8.2f}]")
+    if len(pu) and len(rv) and len(cs):
+        line += (f" push_done max {pu.max() / 1e3:8.2f} recv_done[min {rv.min() / 1e3:8.2f} max {rv.max() / 1e3:8.2f}]"
+                 f" stores_done max {cs.max() / 1e3:8.2f}")
     if prev_end is not None:
         line += f"  dt(exit-exit) {(en.max() - prev_end) / 1e3:6.2f}"
     prev_end = en.max()
