@@ -175,6 +175,8 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *  "pdl"      programmatic dependent launch between the kernels of a task (default 1)
  *  "splitk"   split-K cluster size of the weight-streaming GEMMs, 0 = automatic (default 0)
  *  "prefetch" L2 prefetch of the next GEMM's weights by the previous GEMM (default 0)
+ *  "l2pf"     each weight-streaming GEMM prefetches its weight tiles beyond the shared-memory
+ *             pipeline depth into L2 before its grid-dependency wait (default 0)
  *  "persistent" run F / F' of all-RESMLP partitions (<= 16-row micro-batches) as ONE cooperative
  *             persistent kernel with grid barriers between phases (default 0)
  * Test-only negative controls (never used on the product path):

@@ -14,46 +14,88 @@ TGP_DEV void store_op(const EpiParams& e, int r, int f, float v) {
     reinterpret_cast<float*>(e.op)[(int64_t)r * e.ld_op + f] = v;
 }
 
-// Applies the epilogue to one accumulator value; returns the value contributed to the column sum
-// (EPI_ACT_BWD), else 0.
+// The epilogue in two halves, specialised on the mode at compile time (the tcgen05 GEMM is
+// instantiated per mode, which keeps its tail a few dozen straight-line instructions: the generic
+// switch cost ~1 us per CTA in instruction-fetch stalls, profiles/gemm_timeline.py).  epi_load gathers
+// everything an output element needs besides its accumulator (bias, residual, saved pre-activation,
+// dropout decision) -- the GEMM issues it during its mainloop, off the kernel's serial tail;
+// epi_finish does the arithmetic and the stores.  epi_apply = both back to back (bit-identical).
+struct EpiPre {
+  float a = 0.0f, b = 0.0f;
+  bool keep = true;
+};
+
+template <int MODE>
+TGP_DEV EpiPre epi_load(const EpiParams& e, int f, int r) {
+  EpiPre q;
+  if constexpr (MODE == EPI_LINEAR_FWD) {
+    q.a = e.bias ? e.bias[f] : 0.0f;
+  } else if constexpr (MODE == EPI_RESID_FWD) {
+    q.a = e.bias ? e.bias[f] : 0.0f;
+    q.b = e.res[(int64_t)r * e.ld_res + f];
+  } else if constexpr (MODE == EPI_ACT_BWD) {
+    if (e.act) q.a = e.zbuf[(int64_t)r * e.ldz + f];
+  }
+  if constexpr (MODE == EPI_LINEAR_FWD || MODE == EPI_ACT_BWD) {
+    if (e.drop_thresh) {
+      const uint64_t idx = (uint64_t)(e.row_global0 + r) * (uint64_t)e.drop_width + (uint64_t)f;
+      q.keep = dropout_keep(e.seed, *e.step, e.site, idx, e.drop_thresh);
+    }
+  }
+  return q;
+}
+
+// Finishes one accumulator value; returns the value contributed to the column sum (EPI_ACT_BWD),
+// else 0.
+template <int MODE>
+TGP_DEV float epi_finish(const EpiParams& e, int f, int r, float v, const EpiPre& q) {
+  if constexpr (MODE == EPI_LINEAR_FWD) {
+    const float z = v + q.a;
+    if (e.zbuf) e.zbuf[(int64_t)r * e.ldz + f] = z;
+    float y = act_f(e.act, z);
+    if (e.drop_thresh) y = q.keep ? y * e.drop_scale : 0.0f;
+    if (e.out0) e.out0[(int64_t)r * e.ld0 + f] = y;
+    if (e.op) store_op(e, r, f, y);
+    return 0.0f;
+  } else if constexpr (MODE == EPI_RESID_FWD) {
+    const float y = v + q.a + q.b;
+    e.out0[(int64_t)r * e.ld0 + f] = y;
+    if (e.op) store_op(e, r, f, y);
+    return 0.0f;
+  } else if constexpr (MODE == EPI_ACT_BWD) {
+    float d = v;
+    if (e.drop_thresh) d = q.keep ? d * e.drop_scale : 0.0f;
+    if (e.act) d *= act_df(e.act, q.a);
+    if (e.op) store_op(e, r, f, d);
+    if (e.out0) e.out0[(int64_t)r * e.ld0 + f] = d;
+    return d;
+  } else if constexpr (MODE == EPI_STORE) {
+    if (f < e.split_f)
+      e.out0[(int64_t)r * e.ld0 + f] = v;
+    else
+      e.out1[(int64_t)r * e.ld1 + (f - e.split_f)] = v;
+    return 0.0f;
+  } else {
+    return 0.0f;
+  }
+}
+
+template <int MODE>
+TGP_DEV float epi_apply(const EpiParams& e, int f, int r, float v) {
+  return epi_finish<MODE>(e, f, r, v, epi_load<MODE>(e, f, r));
+}
+
+// Runtime-mode dispatch (fp32 SIMT GEMM).
 TGP_DEV float epi_apply(const EpiParams& e, int f, int r, float v) {
   switch (e.mode) {
-    case EPI_LINEAR_FWD: {
-      float z = v + (e.bias ? e.bias[f] : 0.0f);
-      if (e.zbuf) e.zbuf[(int64_t)r * e.ldz + f] = z;
-      float y = act_f(e.act, z);
-      if (e.drop_thresh) {
-        uint64_t idx = (uint64_t)(e.row_global0 + r) * (uint64_t)e.drop_width + (uint64_t)f;
-        y = dropout_keep(e.seed, *e.step, e.site, idx, e.drop_thresh) ? y * e.drop_scale : 0.0f;
-      }
-      if (e.out0) e.out0[(int64_t)r * e.ld0 + f] = y;
-      if (e.op) store_op(e, r, f, y);
-      return 0.0f;
-    }
-    case EPI_RESID_FWD: {
-      float y = v + (e.bias ? e.bias[f] : 0.0f) + e.res[(int64_t)r * e.ld_res + f];
-      e.out0[(int64_t)r * e.ld0 + f] = y;
-      if (e.op) store_op(e, r, f, y);
-      return 0.0f;
-    }
-    case EPI_ACT_BWD: {
-      float d = v;
-      if (e.drop_thresh) {
-        uint64_t idx = (uint64_t)(e.row_global0 + r) * (uint64_t)e.drop_width + (uint64_t)f;
-        d = dropout_keep(e.seed, *e.step, e.site, idx, e.drop_thresh) ? d * e.drop_scale : 0.0f;
-      }
-      if (e.act) d *= act_df(e.act, e.zbuf[(int64_t)r * e.ldz + f]);
-      if (e.op) store_op(e, r, f, d);
-      if (e.out0) e.out0[(int64_t)r * e.ld0 + f] = d;
-      return d;
-    }
-    case EPI_STORE: {
-      if (f < e.split_f)
-        e.out0[(int64_t)r * e.ld0 + f] = v;
-      else
-        e.out1[(int64_t)r * e.ld1 + (f - e.split_f)] = v;
-      return 0.0f;
-    }
+    case EPI_LINEAR_FWD:
+      return epi_apply<EPI_LINEAR_FWD>(e, f, r, v);
+    case EPI_RESID_FWD:
+      return epi_apply<EPI_RESID_FWD>(e, f, r, v);
+    case EPI_ACT_BWD:
+      return epi_apply<EPI_ACT_BWD>(e, f, r, v);
+    case EPI_STORE:
+      return epi_apply<EPI_STORE>(e, f, r, v);
     default:
       return 0.0f;
   }

@@ -15,7 +15,7 @@ namespace tgp {
 
 #ifdef TGP_GEMM_TIMING
 // Debug instrumentation (variant builds only): per-CTA %globaltimer stamps of the last launches.
-__device__ unsigned long long g_ts[8192][8];
+__device__ unsigned long long g_ts[8192][12];
 __device__ unsigned int g_ts_next;
 TGP_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -52,7 +52,7 @@ struct TcCfg {
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int MODE>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                    const __grid_constant__ CUtensorMap tmB1, const GemmParams p) {
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    if (C::PUSH && p.epi.mode != EPI_DW) {
+    if (C::PUSH && MODE != EPI_DW) {
       // every byte of the receive region is written once by the S cluster ranks' st.async
       mbar_init(rbar, 1);
       fence_barrier_init();
@@ -104,9 +104,12 @@ __global__ void __launch_bounds__(192, 1)
   griddep_launch();
   // receive barriers of all cluster ranks must be initialised before anyone pushes into them:
   // arrive now, wait right before the first push (the whole mainloop in between)
-  const bool push_red = C::PUSH && p.epi.mode != EPI_DW;
+  constexpr bool push_red = C::PUSH && MODE != EPI_DW;
   if (push_red) cluster_arrive();
 
+  // owner-epilogue operands gathered during the mainloop (PUSH tiles, first PRE_IT items/thread)
+  constexpr int PRE_IT = 2;
+  EpiPre pre[PRE_IT][4];
   auto stage_a = [&](int s) { return smem + s * C::STAGE; };
   auto stage_b = [&](int s) { return smem + s * C::STAGE + C::A_BYTES; };
   const int m0 = m_tile * 128;
@@ -145,6 +148,17 @@ __global__ void __launch_bounds__(192, 1)
         for (int it = 0; it < pre; ++it) {
           mbar_arrive_expect_tx(&full[it], C::STAGE);
           load_a(it, kb0 + it);
+        }
+        if (p.a_l2pf) {
+          for (int it = pre; it < nkb; ++it) {
+            const int k = (kb0 + it) * C::BK;
+            if (A_MN) {
+              tma_prefetch_l2_2d(&tmA, m0, k);
+              tma_prefetch_l2_2d(&tmA, m0 + 64, k);
+            } else {
+              tma_prefetch_l2_2d(&tmA, k, m0);
+            }
+          }
         }
       }
       griddep_wait();
@@ -204,13 +218,30 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // ---------------- epilogue warps 2..5: TMEM -> registers
     griddep_wait();
+    if (push_red) {
+      // gather the owner-side epilogue operands (bias, residual, pre-activation, dropout mask) now,
+      // while the mainloop streams: the tail after the split-K exchange is then arithmetic + stores
+      const int S = gridDim.y, lrpr = 8 - __ffs(S), rpr = 1 << lrpr, rank = (int)cluster_ctarank();
+      const int et = (int)threadIdx.x - 64;
+      const int nvalid = min(BN, p.N - nb), nq = (nvalid + 3) >> 2;
+#pragma unroll
+      for (int t = 0; t < PRE_IT; ++t) {
+        const int it = et + 128 * t;
+        if (it < rpr * nq) {
+          const int fll = it & (rpr - 1), q = it >> lrpr, f = m0 + rank * rpr + fll;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (f < p.M && 4 * q + e < nvalid) pre[t][e] = epi_load<MODE>(p.epi, f, nb + 4 * q + e);
+        }
+      }
+    }
     mbar_wait(tfull, 0);
     tc_fence_after();
     if (threadIdx.x == 64) TGP_TS(3);
     const int lg = warp & 3;  // TMEM lane group accessible to this warp
     const int fl = lg * 32 + lane;
     const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
-    if (p.epi.mode == EPI_DW) {
+    if constexpr (MODE == EPI_DW) {
       const EpiParams& e = p.epi;
       const int m = m0 + fl;
       float* row = e.dw + (int64_t)m * e.ldw + nb;
@@ -238,12 +269,12 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
-    } else if (C::PUSH) {
+    } else if constexpr (C::PUSH) {
       // push: every rank STORES the slice of its partial tile owned by rank `owner` (features
       // [owner*rpr, +rpr)) into the owner's dedicated receive region, slot = source rank:
       // quad (src, c, fll, q) at float4 ((src*(BN/16) + c)*rpr + fll)*4 + (q ^ (fll & 3)).
-      const int S = gridDim.y, rpr = 128 / S;
-      const int owner = fl / rpr, fll = fl % rpr, src = (int)cluster_ctarank();
+      const int lrpr = 8 - __ffs((int)gridDim.y), rpr = 1 << lrpr;  // split S = 128 / rpr, a power of two
+      const int owner = fl >> lrpr, fll = fl & (rpr - 1), src = (int)cluster_ctarank();
       const uint32_t recv = smem_u32(smem + C::DATA);
       const uint32_t rmbar = mapa_shared(smem_u32(rbar), (uint32_t)owner);
       cluster_wait();  // every rank's receive barrier is initialised (arrived right after setup)
@@ -278,23 +309,25 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
 
-  if (p.epi.mode != EPI_DW && C::PUSH) {
+  if constexpr (MODE != EPI_DW && C::PUSH) {
     // ---------------- wait for the S ranks' partials (local mbarrier), then a purely local
     // fixed-order (source-rank) sum
     if (threadIdx.x >= 64) mbar_wait(rbar, 0);
     if (threadIdx.x == 64) TGP_TS(6);
     const int S = gridDim.y;
     const int rank = (int)cluster_ctarank();
-    const int rpr = 128 / S;
+    const int lrpr = 8 - __ffs(S), rpr = 1 << lrpr;  // S is a power of two <= 8
     const int et = (int)threadIdx.x - 64;
     const int nvalid = min(BN, p.N - nb);
     const int nq = (nvalid + 3) >> 2;
     const float4* recv4 = reinterpret_cast<const float4*>(smem + C::DATA);
     float* cs = reinterpret_cast<float*>(smem + C::DATA + C::RECV_BYTES);
-    const bool want_cs = p.epi.mode == EPI_ACT_BWD && p.epi.colsum;
+    const bool want_cs = MODE == EPI_ACT_BWD && p.epi.colsum;
     if (et >= 0) {
-      for (int it = et; it < rpr * nq; it += 128) {
-        const int fll = it % rpr, q = it / rpr;
+      // one work item = (feature, 4-row quad): fixed source-rank order sum, then the epilogue with
+      // the operands gathered during the mainloop (items past PRE_IT per thread load them here)
+      auto item = [&](int it, const EpiPre* pq) {
+        const int fll = it & (rpr - 1), q = it >> lrpr;
         const int f = m0 + rank * rpr + fll;
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int s = 0; s < S; ++s) {
@@ -305,14 +338,23 @@ __global__ void __launch_bounds__(192, 1)
           a.w += t.w;
         }
         const float av[4] = {a.x, a.y, a.z, a.w};
+        if (threadIdx.x == 64 && it == et) TGP_TS(8);
         float part = 0.0f;
         if (f < p.M) {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (4 * q + e < nvalid) part += epi_apply(p.epi, f, nb + 4 * q + e, av[e]);
+            if (4 * q + e < nvalid)
+              part += pq ? epi_finish<MODE>(p.epi, f, nb + 4 * q + e, av[e], pq[e])
+                        : epi_apply<MODE>(p.epi, f, nb + 4 * q + e, av[e]);
         }
         if (want_cs) cs[q * rpr + fll] = part;
-      }
+        if (threadIdx.x == 64 && it == et) TGP_TS(9);
+      };
+#pragma unroll
+      for (int t = 0; t < PRE_IT; ++t)
+        if (et + 128 * t < rpr * nq) item(et + 128 * t, pre[t]);
+#pragma unroll 1
+      for (int it = et + 128 * PRE_IT; it < rpr * nq; it += 128) item(it, nullptr);
       if (want_cs) {
         asm volatile("bar.sync 1, 128;" ::: "memory");  // the 128 epilogue threads only
         if (et < rpr) {
@@ -324,23 +366,23 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
     if (threadIdx.x == 64) TGP_TS(7);
-  } else if (p.epi.mode != EPI_DW) {
+  } else if constexpr (MODE != EPI_DW) {
     // ---------------- deterministic split-K reduction through DSMEM, fixed rank order.
     // Rank r finalises features [r*128/S, (r+1)*128/S); work item = (feature, 4-row quad); all S
     // remote quads are requested before the fixed-order sum.
     cluster_sync();
     const int S = gridDim.y;
     const int rank = (int)cluster_ctarank();
-    const int rpr = 128 / S;
+    const int lrpr = 8 - __ffs(S), rpr = 1 << lrpr;  // S is a power of two <= 8
     const int et = (int)threadIdx.x - 64;
     const int nvalid = min(BN, p.N - nb);
     const int nq = (nvalid + 3) >> 2;
     float* cs = reinterpret_cast<float*>(smem + C::RED_BYTES);  // [q][feature] column-sum partials
-    const bool want_cs = p.epi.mode == EPI_ACT_BWD && p.epi.colsum;
+    const bool want_cs = MODE == EPI_ACT_BWD && p.epi.colsum;
     if (et >= 0) {
       const uint32_t base = smem_u32(smem);
       for (int it = et; it < rpr * nq; it += 128) {
-        const int fll = it % rpr, q = it / rpr;
+        const int fll = it & (rpr - 1), q = it >> lrpr;
         const int fl = rank * rpr + fll;
         const int f = m0 + fl;
         const uint32_t off = (uint32_t)(((q >> 2) * 128 + fl) * 4 + ((q & 3) ^ (fl & 3))) * 16u;
@@ -362,7 +404,7 @@ __global__ void __launch_bounds__(192, 1)
         if (f < p.M) {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (4 * q + e < nvalid) part += epi_apply(p.epi, f, nb + 4 * q + e, av[e]);
+            if (4 * q + e < nvalid) part += epi_apply<MODE>(p.epi, f, nb + 4 * q + e, av[e]);
         }
         if (want_cs) cs[q * rpr + fll] = part;
       }
@@ -403,11 +445,11 @@ bool make_map(CUtensorMap* map, const TcMat& t, int box_inner, int box_outer) {
   return true;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int MODE>
 static int launch_tc(cudaStream_t st, bool pdl, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
                      const GemmParams& p, int S, int ntiles) {
   using C = TcCfg<BN>;
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, MODE>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -494,21 +536,32 @@ int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B
   } else {
     mb1 = mb0;
   }
-#define TGP_LAUNCH(BNv)                                                                    \
-  if (BN == BNv) {                                                                         \
-    if (!a_mn && !b_mn) return launch_tc<BNv, false, false>(st, pdl, ma, mb0, mb1, p, S, ntiles); \
-    if (a_mn && !b_mn) return launch_tc<BNv, true, false>(st, pdl, ma, mb0, mb1, p, S, ntiles);   \
-    if (a_mn && b_mn) return launch_tc<BNv, true, true>(st, pdl, ma, mb0, mb1, p, S, ntiles);     \
-  }
+  // instantiated for the (operand majors, epilogue mode) pairs the runtime uses: forward
+  // W[out][in] x X[rows][in] (K-major, K-major), backward W^T x dY (MN-major, K-major), deferred dW
+  // dY^T x X (MN-major, MN-major)
+  const int mode = p.epi.mode;
+#define TGP_LAUNCH_M(BNv, AM, BM, MD) \
+  if (BN == BNv && a_mn == AM && b_mn == BM && mode == MD) return launch_tc<BNv, AM, BM, MD>(st, pdl, ma, mb0, mb1, p, S, ntiles);
+#define TGP_LAUNCH(BNv)                                  \
+  TGP_LAUNCH_M(BNv, false, false, EPI_LINEAR_FWD)        \
+  TGP_LAUNCH_M(BNv, false, false, EPI_RESID_FWD)         \
+  TGP_LAUNCH_M(BNv, false, false, EPI_STORE)             \
+  TGP_LAUNCH_M(BNv, true, false, EPI_ACT_BWD)            \
+  TGP_LAUNCH_M(BNv, true, false, EPI_STORE)
   if (!dw) {
     TGP_LAUNCH(16)
     TGP_LAUNCH(32)
+    TGP_LAUNCH(64)
+    TGP_LAUNCH(128)
+    TGP_LAUNCH(256)
+  } else {
+    TGP_LAUNCH_M(64, true, true, EPI_DW)
+    TGP_LAUNCH_M(128, true, true, EPI_DW)
+    TGP_LAUNCH_M(256, true, true, EPI_DW)
   }
-  TGP_LAUNCH(64)
-  TGP_LAUNCH(128)
-  TGP_LAUNCH(256)
+#undef TGP_LAUNCH_M
 #undef TGP_LAUNCH
-  set_error("gemm_tc: no instantiation for BN=%d a_mn=%d b_mn=%d", BN, (int)a_mn, (int)b_mn);
+  set_error("gemm_tc: no instantiation for BN=%d a_mn=%d b_mn=%d mode=%d", BN, (int)a_mn, (int)b_mn, mode);
   return -5;
 }
 
@@ -519,7 +572,7 @@ extern "C" int tgp_debug_timestamps(unsigned long long* out, int cap, int reset)
   unsigned int n = 0;
   cudaMemcpyFromSymbol(&n, tgp::g_ts_next, 4);
   const int m = (int)(n < (unsigned)cap ? n : (unsigned)cap);
-  cudaMemcpyFromSymbol(out, tgp::g_ts, (size_t)m * 8 * 8);
+  cudaMemcpyFromSymbol(out, tgp::g_ts, (size_t)m * 12 * 8);
   if (reset) {
     unsigned int z = 0;
     cudaMemcpyToSymbol(tgp::g_ts_next, &z, 4);

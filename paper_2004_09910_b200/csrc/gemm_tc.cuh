@@ -66,6 +66,9 @@ struct GemmParams {
   int k_seg;          // k >= k_seg reads B from the second tensor map (concat-merge), else K
   int kb_per_split;   // k-blocks handled by each cluster rank (split-K)
   int a_is_weight;    // A does not depend on the previous kernel (prefetch before griddep wait)
+  // weight tiles beyond the smem pipeline depth are prefetched into L2 before the griddep wait
+  // (HBM keeps streaming this kernel's weights while the previous kernel drains its epilogue)
+  int a_l2pf;
   // L2 prefetch of the NEXT GEMM's weight matrix (the task's GEMM sequence is static): every CTA
   // prefetches its 1/grid share after issuing its own loads, so HBM keeps streaming across the
   // kernel boundary (epilogue / launch / prologue of the next GEMM).  pf_bytes = 0: none.

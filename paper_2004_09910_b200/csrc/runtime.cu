@@ -165,6 +165,7 @@ static int run_gemm(tgp_ctx* c, Stage& s, bool pdl, Opnd A, bool a_mn, Opnd B0, 
   p.n0 = n0;
   p.k_seg = B1 ? k_seg : K;
   p.a_is_weight = a_weight ? 1 : 0;
+  p.a_l2pf = a_weight && c->l2pf ? 1 : 0;
   p.epi = e;
   c->kernels += 1;
   if (c->bf16) {

@@ -137,6 +137,7 @@ struct tgp_ctx {
   // persistent forward-task kernel: opt-in (measured 0.93 ms vs 0.86 ms per F task at C2 n = 1;
   // five ~2 us grid barriers per block dominate -- profiles/pt_phases.py)
   bool use_graphs = true, use_pdl = true, trace = false, poison = false, prefetch = false, persistent = false;
+  bool l2pf = false;
   int splitk = 0, skip_wait_part = -1;
   uint64_t delay_push_ns = 0;
   bool can_flush = false;

@@ -24,12 +24,21 @@ f = lib.tgp_debug_timestamps
 f.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
 f.restype = ctypes.c_int
 P.bench_dominant_gemm(0, 512, reps=1)  # warm
-buf = np.zeros((8192, 8), dtype=np.uint64)
+buf = np.zeros((8192, 12), dtype=np.uint64)
 f(buf.ctypes.data, 8192, 1)
 ms, by, n = P.bench_dominant_gemm(0, 512, reps=1)
 cnt = f(buf.ctypes.data, 8192, 1)
 ncta = 32 * sk
 rows = buf[:cnt].astype(np.int64)
+own = rows[:, 6] > 0
+for a_, b_, nm in ((3, 6, "tfull->recv"), (6, 8, "recv->sum"), (8, 9, "sum->epi_done"), (9, 7, "epi_done->stores"),
+                   (7, 4, "stores->exit"), ):
+    d = rows[own, b_] - rows[own, a_]
+    if rows[own, b_].min() == 0:
+        continue
+    print(f"{nm:18s} ns pct0/50/90/100", np.percentile(d, [0, 50, 90, 100]))
+if len(sys.argv) > 2:
+    np.save(sys.argv[2], rows)
 # drop the warm-up round (first 32 launches) recorded in this window
 launches = cnt // ncta
 print(f"splitk={sk} chain avg {ms * 1e3:.2f} us/launch, {launches} launches recorded, {ncta} CTAs each")
