@@ -173,6 +173,9 @@ def run_tgp(args):
     if ws > 1:
         from paper_2004_09910_b200.dist import connect_pipeline
         connect_pipeline(P, rank, ws)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        P.set_option(k, int(v))
     P.init_params(seed=1234)
     first, last = rank == 0, rank == n - 1
     g = torch.Generator(device="cpu").manual_seed(1234)
@@ -274,6 +277,7 @@ def main():
     ap.add_argument("--lr", type=float, default=0.05)
     ap.add_argument("--ref-blocks", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--opt", action="append", default=[], help="runtime option name=value (tgp_set_option)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -15,6 +15,7 @@
 #include "host.h"
 #include "runtime.h"
 #include "task_fwd.h"
+#include "task_stream.h"
 
 using namespace tgp;
 
@@ -297,8 +298,93 @@ static int exec_forward_persistent(tgp_ctx* c, Stage& s, int i, int r0, int M) {
   return task_fwd_launch(s.comp, t, s.pt_grid);
 }
 
+// Persistent weight-streaming task kernel (task_stream.cu): layer descriptors (tensor maps of the
+// weights and operand stashes) and per-(micro-batch, block) pointers, (re)built when B changes.
+static int st_build_desc(tgp_ctx* c, Stage& s, int B) {
+  const int L = s.l1 - s.l0;
+  std::vector<SLayer> hl((size_t)L);
+  for (int l = s.l0; l < s.l1; ++l) {
+    LayerRT& Ly = c->layers[l];
+    const int d = Ly.L.d_in, H = Ly.L.d_hidden;
+    SLayer& P = hl[(size_t)(l - s.l0)];
+    memset(&P, 0, sizeof(P));
+    const void* w1 = wparam(c, s, Ly, 2);
+    const void* w2 = wparam(c, s, Ly, 4);
+    if (!make_map(&P.w1k, TcMat{w1, H, d, d}, 64, 128) || !make_map(&P.w2k, TcMat{w2, d, H, H}, 64, 128) ||
+        !make_map(&P.w2m, TcMat{w2, d, H, H}, 64, 64) || !make_map(&P.w1m, TcMat{w1, H, d, d}, 64, 64) ||
+        !make_map(&P.hop, TcMat{Ly.Hop, c->max_batch, d, d}, 64, 16) ||
+        !make_map(&P.gop, TcMat{Ly.Gop, c->max_batch, H, H}, 64, 16) ||
+        !make_map(&P.dyop, TcMat{Ly.dYop, c->max_batch, d, d}, 64, 16) ||
+        !make_map(&P.daop, TcMat{Ly.dAop, c->max_batch, H, H}, 64, 16))
+      return TGP_E_CUDA;
+    P.gamma = mparam(s, Ly, 0);
+    P.beta = mparam(s, Ly, 1);
+    P.b1 = mparam(s, Ly, 3);
+    P.b2 = mparam(s, Ly, 5);
+    P.drop_thresh = drop_thresh(Ly.L.dropout);
+    P.drop_scale = Ly.L.dropout > 0 ? 1.0f / (1.0f - Ly.L.dropout) : 1.0f;
+    P.site = (uint32_t)l;
+  }
+  std::vector<SMicro> hm((size_t)c->m * L);
+  for (int i = 1; i <= c->m; ++i) {
+    int r0 = 0, M = 0;
+    micro_rows(c, B, i, &r0, &M);
+    const int slot = c->slot_of[i];
+    for (int l = s.l0; l < s.l1; ++l) {
+      LayerRT& Ly = c->layers[l];
+      const int d = Ly.L.d_in, H = Ly.L.d_hidden;
+      SMicro& P = hm[(size_t)(i - 1) * L + (l - s.l0)];
+      P.x = (l == s.l0) ? s.self.fwd_in + (size_t)r0 * d : c->layers[l - 1].out[slot];
+      P.y = (l == s.l1 - 1) ? s.out + (size_t)r0 * d : Ly.out[slot];
+      P.a = Ly.z[slot];
+      P.mean = Ly.mean[slot];
+      P.rstd = Ly.rstd[slot];
+      P.hop = (__nv_bfloat16*)opptr(c, Ly.Hop, r0, d);
+      P.gop = (__nv_bfloat16*)opptr(c, Ly.Gop, r0, H);
+      P.dyop = (__nv_bfloat16*)opptr(c, Ly.dYop, r0, d);
+      P.daop = (__nv_bfloat16*)opptr(c, Ly.dAop, r0, H);
+      const size_t po = (size_t)(i - 1) * c->pb;
+      P.pb = Ly.pb + po * H;
+      P.pb2 = Ly.pb2 + po * d;
+      P.pg = Ly.pg + po * d;
+      P.pbt = Ly.pbt + po * d;
+    }
+  }
+  TGP_CUDA_TRY(cudaMemcpyAsync(s.st_layers, hl.data(), hl.size() * sizeof(SLayer), cudaMemcpyHostToDevice, s.comp));
+  TGP_CUDA_TRY(cudaMemcpyAsync(s.st_micro, hm.data(), hm.size() * sizeof(SMicro), cudaMemcpyHostToDevice, s.comp));
+  TGP_CUDA_TRY(cudaStreamSynchronize(s.comp));
+  s.st_micro_B = B;
+  return 0;
+}
+
+static bool use_stream(const tgp_ctx* c, const Stage& s, int M) { return s.st_ok && c->stream && M <= 16; }
+
+static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd) {
+  const LayerRT& L0 = c->layers[s.l0];
+  STask t{};
+  t.L = s.l1 - s.l0;
+  t.layers = (const SLayer*)s.st_layers;
+  t.micro = (const SMicro*)s.st_micro + (size_t)(i - 1) * t.L;
+  t.d = L0.L.d_in;
+  t.H = L0.L.d_hidden;
+  t.M = M;
+  t.r0 = r0;
+  t.bwd = bwd ? 1 : 0;
+  t.gy_top = s.self.grad_in + (size_t)r0 * s.d_out;
+  t.dx_bottom = s.dx_out + (size_t)r0 * s.d_in;
+  t.gbuf0 = s.gbuf[0];
+  t.gbuf1 = s.gbuf[1];
+  t.stats = s.st_stats;
+  t.cnt = s.st_cnt;
+  t.seed = c->seed;
+  t.step = s.dstep;
+  c->kernels += 2;  // counter reset + task kernel
+  return task_stream_launch(s.comp, t, s.st_clusters);
+}
+
 // F_{i,j} (and F'_{i,j}: identical kernels and launch configuration -> bitwise identical output)
 static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
+  if (use_stream(c, s, M)) return exec_task_stream(c, s, i, r0, M, false);
   if (s.pt_ok && c->persistent && M <= 16) return exec_forward_persistent(c, s, i, r0, M);
   const int slot = c->slot_of[i];
   float* x = s.self.fwd_in + (size_t)r0 * s.d_in;
@@ -406,6 +492,7 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
 // B_{i,j}: VJPs through the partition's layers in reverse; stashes dW operands, per-micro-batch
 // column partials (bias / LN / BN grads), writes dx rows (message source) and skip gradients.
 static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
+  if (use_stream(c, s, M)) return exec_task_stream(c, s, i, r0, M, true);
   const int slot = c->slot_of[i];
   float* g = s.self.grad_in + (size_t)r0 * s.d_out;
   int pp = 0;
@@ -739,6 +826,7 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       }
       cudaEvent_t ta = nullptr;
       trace_begin(c, s, s.comp, 0, rc.kind, i, &ta);
+      if (use_stream(c, s, M) && s.st_micro_B != B) TGP_TRY(st_build_desc(c, s, B));
       if (rc.kind == K_B) {
         TGP_TRY(run_task(c, s, s.gB[i - 1], B, [&] { return exec_backward(c, s, i, r0, M); }));
         TGP_CUDA_TRY(cudaEventRecord(s.bdone[i - 1], s.comp));

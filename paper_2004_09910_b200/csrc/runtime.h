@@ -101,6 +101,14 @@ struct Stage {
   unsigned* pt_bar = nullptr;
   int pt_grid = 0;
   void* pt_dbg = nullptr;
+  // persistent weight-streaming task kernel (task_stream.cu): F / F' / B of all-RESMLP partitions
+  bool st_ok = false;
+  int st_clusters = 0;
+  void* st_layers = nullptr;  // device SLayer[L]
+  void* st_micro = nullptr;   // device SMicro[m][L]
+  int st_micro_B = -1;
+  float* st_stats = nullptr;
+  unsigned* st_cnt = nullptr;
   std::vector<TaskGraph> gF, gB;
   TaskGraph gW;
   bool grads_fresh = true;
@@ -138,6 +146,7 @@ struct tgp_ctx {
   // five ~2 us grid barriers per block dominate -- profiles/pt_phases.py)
   bool use_graphs = true, use_pdl = true, trace = false, poison = false, prefetch = false, persistent = false;
   bool l2pf = false;
+  bool stream = true;  // persistent weight-streaming task kernel where eligible (task_stream.cu)
   int splitk = 0, skip_wait_part = -1;
   uint64_t delay_push_ns = 0;
   bool can_flush = false;

@@ -1,0 +1,612 @@
+// Persistent weight-streaming task kernel: ONE launch executes a whole GPipe compute task of a
+// partition made of pre-LN residual MLP blocks -- F_{i,j} / F'_{i,j} (PAPER.md Eq. F_{i,j},
+// P:52-55; recompute P:105) or B_{i,j} (Eq. B_{i,j}) -- for one micro-batch of
+// M <= 16 rows.
+//
+// Why: at 16 rows per micro-batch every dense layer is a weight-streaming GEMM (arithmetic
+// intensity 15.9 FLOP/B): the task is a chain of 2 dependent 32 MiB weight reads
+// per block.  As separate kernels, every boundary drains and refills the HBM pipe.  Here the weight
+// stream of every CTA is static and independent of the activations, so it runs ahead continuously
+// across all GEMMs of the task through a 10-stage TMA ring; only the tiny activation operand of a
+// GEMM waits for its producers.
+//
+// Work split (grid = C clusters x 4 CTAs, one CTA per SM, C = max(d, H) / 128 <= 37):
+//  * every GEMM phase has out-features F (H or d) in 128-row slabs; cluster c owns slab c, its 4
+//    CTAs split K in quarters (swap-AB tcgen05.mma M = 128 features x N = 16 rows, fp32 in TMEM);
+//  * split-K partials are reduced inside the cluster: each rank pushes 32-feature slices of its
+//    TMEM tile into the owning rank's shared memory with st.async (completion on the owner's
+//    mbarrier); the owner sums the 4 sources in fixed rank order (deterministic -> F' == F
+//    bitwise, reading Z21) and runs the epilogue for its 32 features x 16 rows;
+//  * dependencies are counters (one 128-byte line each): an owner signals "my 32 outputs of
+//    phase p are written" with a release increment on the counter of the K-quarter they fall in;
+//    a CTA of the next phase polls only the counter of its own K-quarter before the TMA load of its
+//    activation operand.  Row reductions (LayerNorm statistics forward, LayerNorm backward sums)
+//    go through per-32-feature chunk statistics and one global counter, combined in fixed order.
+//
+// Phases.  Forward, block l (ids are dependency counters):
+//   [l = 0] LN(x) statistics (id 0) -> h_0 = LN(x) bf16 (id 1)
+//   GEMM1 a = h W1^T + b1 -> g = dropout(GELU(a)) bf16        (id 2 + 3l)
+//   GEMM2 y = x + g W2^T + b2 -> [l < L-1] stats (id 3 + 3l) -> h_{l+1} = LN(y) (id 4 + 3l)
+// Backward, k = 0..L-1 over blocks l = L-1-k:
+//   [k = 0] dY_top bf16 + db2 column sums (id 1)
+//   dG = dY W2 -> dA = dG * dropout' * GELU'(a) bf16, db1 column sums       (id 2 + 3k)
+//   dH = dA W1 -> LN backward row sums (id 3 + 3k) -> dx = gy + LN_bwd(dH);
+//                 dgamma, dbeta column sums; [l > 0] dY_{l-1} = dx bf16, db2 sums (id 4 + 3k)
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "host.h"
+#include "kernels.h"
+#include "task_stream.h"
+
+namespace tgp {
+
+namespace {
+constexpr int SK = 4;                       // split-K ranks per cluster
+constexpr int ST_A = 16384;                 // 128 x 64 bf16 weight tile (one ring stage)
+constexpr int ST_B = 2048;                  // 16 x 64 bf16 activation tile
+constexpr int ST_STAGES = 10;               // weight ring depth
+constexpr int ST_BT = 16;                   // max k-blocks per rank per phase (K <= 4096)
+constexpr int ST_RECV = SK * 32 * 16 * 4;   // owner receive buffer: [src][32 features][16 rows] fp32
+constexpr int OFF_B = ST_STAGES * ST_A;
+constexpr int OFF_RECV = OFF_B + ST_BT * ST_B;
+constexpr int OFF_BAR = OFF_RECV + 2 * ST_RECV;
+constexpr int ST_SMEM = OFF_BAR + 2048 + 1024;
+constexpr int CNT_STRIDE = 32;              // uints between counters (one 128-byte line each)
+}  // namespace
+
+TGP_DEV unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+TGP_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+template <typename T>
+TGP_DEV T wsum32(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct Ph {
+  const CUtensorMap* A;
+  const CUtensorMap* B;
+  int K, F;
+};
+
+TGP_DEV Ph phase_of(const STask& t, int p) {
+  const int k = p >> 1, sub = p & 1;
+  const int l = t.bwd ? t.L - 1 - k : k;
+  const SLayer& Ly = t.layers[l];
+  if (!t.bwd) return sub ? Ph{&Ly.w2k, &Ly.gop, t.H, t.d} : Ph{&Ly.w1k, &Ly.hop, t.d, t.H};
+  return sub ? Ph{&Ly.w1m, &Ly.daop, t.H, t.d} : Ph{&Ly.w2m, &Ly.dyop, t.d, t.H};
+}
+
+__global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_constant__ STask t) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;
+  uint8_t* bbuf = smem + OFF_B;
+  float* recv = reinterpret_cast<float*>(smem + OFF_RECV);  // [2][SK][32][16]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* empty = full + ST_STAGES;
+  uint64_t* tfull = empty + ST_STAGES;  // [2] TMEM accumulator ready
+  uint64_t* tempty = tfull + 2;         // [2] TMEM accumulator drained (128 arrivals)
+  uint64_t* bfull = tempty + 2;         // activation tiles of a phase landed
+  uint64_t* bempty = bfull + 1;         // MMAs of a phase done (activation buffer reusable)
+  uint64_t* rbar = bempty + 1;          // [2] split-K partials of a phase received (owner)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
+  float* rmu = reinterpret_cast<float*>(smem + OFF_BAR + 512);  // [16] row statistics
+  float* rrs = rmu + 16;                                        // [16]
+  float* cs = rrs + 16;                                         // [3][4][32] column-sum partials
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();
+  const int slab = blockIdx.x / SK;
+  const int NP = 2 * t.L;
+  const int d = t.d, H = t.H, M = t.M;
+  auto active = [&](int p) { return slab * 128 < phase_of(t, p).F; };
+  auto cnt = [&](int id, int q) { return t.cnt + ((size_t)id * 5 + q) * CNT_STRIDE; };
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < ST_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+      mbar_init(&rbar[b], 1);
+    }
+    mbar_init(bfull, 1);
+    mbar_init(bempty, 1);
+    fence_barrier_init();
+    // first use of each receive buffer: 4 sources x 32 features x 16 rows x 4 B
+    mbar_arrive_expect_tx(&rbar[0], ST_RECV);
+    mbar_arrive_expect_tx(&rbar[1], ST_RECV);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 32);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // every rank's receive barriers are initialised before any st.async
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // ------------------------------------------------------------ TMA producer
+      const uint64_t pol_w = policy_evict_first(), pol_b = policy_evict_last();
+      auto next_active = [&](int p) {
+        while (p < NP && !active(p)) ++p;
+        return p;
+      };
+      int wp = next_active(0), wkb = 0, it = 0;  // weight cursor: phase, k-block, ring tile
+      int bp = next_active(0), nb = 0;           // next phase whose activation tiles to load
+      while (wp < NP || bp < NP) {
+        bool progress = false;
+        // poll the dependency of the next activation load (issued first, used after the weight loop)
+        unsigned have = 0, need = 0;
+        const unsigned* dep = nullptr;
+        const bool b_free = bp < NP && (nb == 0 || mbar_test_wait(smem_u32(bempty), (uint32_t)((nb - 1) & 1)));
+        if (b_free) {
+          dep = cnt(1 + 3 * (bp >> 1) + (bp & 1), rank);
+          need = (unsigned)(phase_of(t, bp).K / 128);
+          have = ld_relaxed_u32(dep);
+        }
+        while (wp < NP) {  // weights: run ahead as far as the ring allows
+          const int s = it % ST_STAGES, r = it / ST_STAGES;
+          if (!mbar_test_wait(smem_u32(&empty[s]), (uint32_t)((r & 1) ^ 1))) break;
+          const Ph P = phase_of(t, wp);
+          const int nkb = P.K / (SK * 64);
+          const int kc = (rank * nkb + wkb) * 64;
+          mbar_arrive_expect_tx(&full[s], ST_A);
+          if (!t.bwd) {
+            tma_load_2d(P.A, &full[s], ring + s * ST_A, kc, slab * 128, pol_w);
+          } else {
+            tma_load_2d(P.A, &full[s], ring + s * ST_A, slab * 128, kc, pol_w);
+            tma_load_2d(P.A, &full[s], ring + s * ST_A + 8192, slab * 128 + 64, kc, pol_w);
+          }
+          ++it;
+          progress = true;
+          if (++wkb == nkb) {
+            wkb = 0;
+            wp = next_active(wp + 1);
+          }
+        }
+        if (dep && have >= need) {
+          fence_acq_rel_gpu();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          const Ph P = phase_of(t, bp);
+          const int nkb = P.K / (SK * 64);
+          mbar_arrive_expect_tx(bfull, (uint32_t)(nkb * ST_B));
+          for (int q = 0; q < nkb; ++q) tma_load_2d(P.B, bfull, bbuf + q * ST_B, (rank * nkb + q) * 64, t.r0, pol_b);
+          ++nb;
+          bp = next_active(bp + 1);
+          progress = true;
+        }
+        if (!progress) __nanosleep(32);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      // ------------------------------------------------------------ MMA issuer (single thread)
+      const uint32_t idesc = t.bwd ? make_idesc_bf16(128, 16, true, false) : make_idesc_bf16(128, 16, false, false);
+      int it = 0, n = 0;
+      for (int p = 0; p < NP; ++p) {
+        if (!active(p)) continue;
+        const int nkb = phase_of(t, p).K / (SK * 64);
+        const int buf = n & 1, u = n >> 1;
+        mbar_wait(&tempty[buf], (uint32_t)((u & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t dacc = tmem + (uint32_t)(buf * 16);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % ST_STAGES, r = it / ST_STAGES;
+          mbar_wait(&full[s], (uint32_t)(r & 1));
+          tc_fence_after();
+          if (kb == 0) {
+            mbar_wait(bfull, (uint32_t)(n & 1));
+            tc_fence_after();
+          }
+          const uint32_t a = smem_u32(ring + s * ST_A), b = smem_u32(bbuf + kb * ST_B);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t ad = t.bwd ? make_sdesc_sw128(a + kk * 2048, 8192, 1024) : make_sdesc_sw128(a + kk * 32, 16, 1024);
+            tc_mma_bf16(dacc, ad, make_sdesc_sw128(b + kk * 32, 16, 1024), idesc, (kb | kk) ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&tfull[buf]);
+        tc_commit(bempty);
+        ++n;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ epilogue warps (128 threads)
+    // Owner item: feature f = slab*128 + rank*32 + lane of the phase's out space, rows 4*ew .. 4*ew+3.
+    const int et = threadIdx.x - 64, ew = et >> 5, lg = warp & 3;
+    const int fo = slab * 128 + rank * 32 + lane;
+    const int chunk = slab * SK + rank;  // 32-feature chunk index of the owner slice
+    int n = 0;
+    auto epi_bar = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+    auto signal = [&](int id, int q) {
+      epi_bar();
+      if (et == 0) {
+        __threadfence();
+        atomicAdd(cnt(id, q), 1u);
+      }
+    };
+    auto wait_cnt = [&](int id, int q, unsigned need) {
+      if (et == 0) {
+        while (ld_relaxed_u32(cnt(id, q)) < need) __nanosleep(32);
+        fence_acq_rel_gpu();
+      }
+      epi_bar();
+    };
+    // column sums over the 16 rows of up to 3 values per thread (fixed order: rows within a quad,
+    // then quads), written by warp 0 of the epilogue to dst[k][fo]
+    auto colsums = [&](const float* v0, const float* v1, const float* v2, float* d0, float* d1, float* d2) {
+      const float* v[3] = {v0, v1, v2};
+      float* dd[3] = {d0, d1, d2};
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        if (v[k]) cs[(k * 4 + ew) * 32 + lane] = ((v[k][0] + v[k][1]) + v[k][2]) + v[k][3];
+      epi_bar();
+      if (ew == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          if (v[k] && dd[k])
+            dd[k][fo] = ((cs[(k * 4) * 32 + lane] + cs[(k * 4 + 1) * 32 + lane]) + cs[(k * 4 + 2) * 32 + lane]) +
+                        cs[(k * 4 + 3) * 32 + lane];
+      }
+      epi_bar();
+    };
+    // result of the current GEMM phase for (fo, 4 rows): TMEM -> push slices to their owners ->
+    // fixed-order sum of the 4 sources
+    auto gemm_result = [&](float* acc) {
+      const int buf = n & 1, u = n >> 1;
+      mbar_wait(&tfull[buf], (uint32_t)(u & 1));
+      tc_fence_after();
+      float v[16];
+      tmem_ld16(tmem + (uint32_t)(buf * 16) + ((uint32_t)(lg * 32) << 16), v);
+      tc_fence_before();
+      mbar_arrive(&tempty[buf]);
+      const uint32_t rb = smem_u32(recv + buf * (ST_RECV / 4));
+      const uint32_t dbar = mapa_shared(smem_u32(&rbar[buf]), (uint32_t)lg);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t idx = (uint32_t)((rank * 32 + lane) * 4 + (q ^ (lane & 3)));
+        st_async_f32x4(mapa_shared(rb + idx * 16u, (uint32_t)lg),
+                       make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]), dbar);
+      }
+      mbar_wait(&rbar[buf], (uint32_t)(u & 1));
+      const float4* r4 = reinterpret_cast<const float4*>(recv + buf * (ST_RECV / 4));
+      float4 a = r4[(0 * 32 + lane) * 4 + (ew ^ (lane & 3))];
+#pragma unroll
+      for (int s = 1; s < SK; ++s) {
+        const float4 b = r4[(s * 32 + lane) * 4 + (ew ^ (lane & 3))];
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+      }
+      // re-arm for this buffer's next use (its pushes come only after every owner signalled
+      // this phase, i.e. after the reads above)
+      if (et == 0) mbar_arrive_expect_tx(&rbar[buf], ST_RECV);
+      acc[0] = a.x;
+      acc[1] = a.y;
+      acc[2] = a.z;
+      acc[3] = a.w;
+      ++n;
+    };
+    // forward LayerNorm of block `l` over d features from the owner values y[4] (rows 4ew..):
+    // chunk statistics (mean, M2) -> global counter id_st -> fixed-order combination (identical in
+    // every CTA) -> h = gamma (y - mu) rstd + beta (bf16), mean / rstd saved for the backward.
+    auto layernorm = [&](const float* y, int l, int id_st, int id_out) {
+      const SLayer& Ly = t.layers[l];
+      const SMicro& Mi = t.micro[l];
+      const int J = d / 32;
+      float* st = t.stats + (size_t)l * J * 32;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float mu = wsum32(y[e]) * (1.0f / 32.0f);
+        const float dv = y[e] - mu;
+        const float m2 = wsum32(dv * dv);
+        if (lane == 0) *reinterpret_cast<float2*>(st + ((size_t)chunk * 16 + 4 * ew + e) * 2) = make_float2(mu, m2);
+      }
+      const float g = Ly.gamma[fo], b = Ly.beta[fo];
+      signal(id_st, 4);
+      wait_cnt(id_st, 4, (unsigned)J);
+      {
+        const int rr = et >> 3, jl = et & 7;
+        float2 sv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int j = jl + 8 * u;
+          sv[u] = j < J ? __ldcg(reinterpret_cast<const float2*>(st + ((size_t)j * 16 + rr) * 2)) : make_float2(0.f, 0.f);
+        }
+        float mu = 0.0f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) mu += sv[u].x;
+        mu += __shfl_xor_sync(0xffffffffu, mu, 4);
+        mu += __shfl_xor_sync(0xffffffffu, mu, 2);
+        mu += __shfl_xor_sync(0xffffffffu, mu, 1);
+        mu /= (float)J;
+        float m2 = 0.0f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (jl + 8 * u < J) {
+            const float dm = sv[u].x - mu;
+            m2 += sv[u].y + 32.0f * dm * dm;
+          }
+        m2 += __shfl_xor_sync(0xffffffffu, m2, 4);
+        m2 += __shfl_xor_sync(0xffffffffu, m2, 2);
+        m2 += __shfl_xor_sync(0xffffffffu, m2, 1);
+        const float rs = 1.0f / sqrtf(m2 / (float)d + 1e-5f);
+        if (jl == 0) {
+          rmu[rr] = mu;
+          rrs[rr] = rs;
+          if (blockIdx.x == 0 && rr < M) {
+            Mi.mean[rr] = mu;
+            Mi.rstd[rr] = rs;
+          }
+        }
+      }
+      epi_bar();
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = 4 * ew + e;
+        if (r < M) Mi.hop[(size_t)r * d + fo] = __float2bfloat16_rn(g * ((y[e] - rmu[r]) * rrs[r]) + b);
+      }
+      signal(id_out, fo / (d / 4));
+    };
+
+    const bool own_d = slab * 128 < d, own_h = slab * 128 < H;
+    if (!t.bwd) {
+      // ---------------------------------------------------------------- forward task
+      if (own_d) {
+        float x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = 4 * ew + e;
+          x[e] = r < M ? __ldcg(t.micro[0].x + (size_t)r * d + fo) : 0.0f;
+        }
+        layernorm(x, 0, 0, 1);
+      }
+      for (int l = 0; l < t.L; ++l) {
+        const SLayer& Ly = t.layers[l];
+        const SMicro& Mi = t.micro[l];
+        if (own_h) {  // GEMM1 epilogue: a = acc + b1; g = dropout(GELU(a))
+          const float b1 = Ly.b1[fo];
+          const uint32_t step = Ly.drop_thresh ? *t.step : 0u;
+          float acc[4];
+          gemm_result(acc);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 4 * ew + e;
+            if (r >= M) continue;
+            const float z = acc[e] + b1;
+            Mi.a[(size_t)r * H + fo] = z;
+            float gv = gelu_f(z);
+            if (Ly.drop_thresh) {
+              const uint64_t idx = (uint64_t)(t.r0 + r) * (uint64_t)H + (uint64_t)fo;
+              gv = dropout_keep(t.seed, step, Ly.site, idx, Ly.drop_thresh) ? gv * Ly.drop_scale : 0.0f;
+            }
+            Mi.gop[(size_t)r * H + fo] = __float2bfloat16_rn(gv);
+          }
+          signal(2 + 3 * l, fo / (H / 4));
+        }
+        if (own_d) {  // GEMM2 epilogue: y = x + acc + b2, then LN of the next block
+          const float b2 = Ly.b2[fo];
+          float xr[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 4 * ew + e;
+            xr[e] = r < M ? __ldcg(Mi.x + (size_t)r * d + fo) : 0.0f;
+          }
+          float acc[4], y[4];
+          gemm_result(acc);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 4 * ew + e;
+            y[e] = r < M ? acc[e] + b2 + xr[e] : 0.0f;
+            if (r < M) Mi.y[(size_t)r * d + fo] = y[e];
+          }
+          if (l + 1 < t.L) layernorm(y, l + 1, 3 + 3 * l, 4 + 3 * l);
+        }
+      }
+    } else {
+      // ---------------------------------------------------------------- backward task
+      const int L = t.L;
+      if (own_d) {  // dY of the top block: bf16 operand + db2 column sums
+        const SMicro& Mi = t.micro[L - 1];
+        float g[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = 4 * ew + e;
+          g[e] = r < M ? __ldcg(t.gy_top + (size_t)r * d + fo) : 0.0f;
+          if (r < M) Mi.dyop[(size_t)r * d + fo] = __float2bfloat16_rn(g[e]);
+        }
+        colsums(g, nullptr, nullptr, Mi.pb2, nullptr, nullptr);
+        signal(1, fo / (d / 4));
+      }
+      for (int k = 0; k < L; ++k) {
+        const int l = L - 1 - k;
+        const SLayer& Ly = t.layers[l];
+        const SMicro& Mi = t.micro[l];
+        if (own_h) {  // dG epilogue: dA = dG * dropout mask * GELU'(a)
+          const uint32_t step = Ly.drop_thresh ? *t.step : 0u;
+          float av[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 4 * ew + e;
+            av[e] = r < M ? Mi.a[(size_t)r * H + fo] : 0.0f;
+          }
+          float acc[4], da[4];
+          gemm_result(acc);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 4 * ew + e;
+            da[e] = 0.0f;
+            if (r >= M) continue;
+            float dg = acc[e];
+            if (Ly.drop_thresh) {
+              const uint64_t idx = (uint64_t)(t.r0 + r) * (uint64_t)H + (uint64_t)fo;
+              dg = dropout_keep(t.seed, step, Ly.site, idx, Ly.drop_thresh) ? dg * Ly.drop_scale : 0.0f;
+            }
+            da[e] = dg * gelu_df(av[e]);
+            Mi.daop[(size_t)r * H + fo] = __float2bfloat16_rn(da[e]);
+          }
+          colsums(da, nullptr, nullptr, Mi.pb, nullptr, nullptr);
+          signal(2 + 3 * k, fo / (H / 4));
+        }
+        if (own_d) {  // dH epilogue: LayerNorm backward + residual
+          const float gam = Ly.gamma[fo];
+          const float* gy = (l == L - 1) ? t.gy_top : (((l + 1) & 1) ? t.gbuf1 : t.gbuf0);
+          float* dx = (l == 0) ? t.dx_bottom : ((l & 1) ? t.gbuf1 : t.gbuf0);
+          float nv[4], gyv[4], rsv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 4 * ew + e;
+            if (r < M) {
+              const float mu = Mi.mean[r];
+              rsv[e] = Mi.rstd[r];
+              nv[e] = (Mi.x[(size_t)r * d + fo] - mu) * rsv[e];
+              gyv[e] = __ldcg(gy + (size_t)r * d + fo);
+            } else {
+              nv[e] = gyv[e] = rsv[e] = 0.0f;
+            }
+          }
+          float dh[4], dhn[4], dn[4];
+          gemm_result(dh);
+          const int J = d / 32;
+          float* st = t.stats + (size_t)k * J * 32;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (4 * ew + e >= M) dh[e] = 0.0f;
+            dhn[e] = dh[e] * nv[e];
+            dn[e] = dh[e] * gam;
+            const float s1 = wsum32(dn[e]);
+            const float s2 = wsum32(dn[e] * nv[e]);
+            if (lane == 0) *reinterpret_cast<float2*>(st + ((size_t)chunk * 16 + 4 * ew + e) * 2) = make_float2(s1, s2);
+          }
+          signal(3 + 3 * k, 4);
+          colsums(dhn, dh, nullptr, Mi.pg, Mi.pbt, nullptr);
+          wait_cnt(3 + 3 * k, 4, (unsigned)J);
+          {
+            const int rr = et >> 3, jl = et & 7;
+            float s1 = 0.0f, s2 = 0.0f;
+            for (int j = jl; j < J; j += 8) {
+              const float2 v = __ldcg(reinterpret_cast<const float2*>(st + ((size_t)j * 16 + rr) * 2));
+              s1 += v.x;
+              s2 += v.y;
+            }
+            s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+            if (jl == 0) {
+              rmu[rr] = s1 / (float)d;
+              rrs[rr] = s2 / (float)d;
+            }
+          }
+          epi_bar();
+          float dxv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 4 * ew + e;
+            dxv[e] = 0.0f;
+            if (r >= M) continue;
+            dxv[e] = gyv[e] + rsv[e] * (dn[e] - rmu[r] - nv[e] * rrs[r]);
+            dx[(size_t)r * d + fo] = dxv[e];
+          }
+          if (l > 0) {
+            const SMicro& Mn = t.micro[l - 1];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int r = 4 * ew + e;
+              if (r < M) Mn.dyop[(size_t)r * d + fo] = __float2bfloat16_rn(dxv[e]);
+            }
+            colsums(dxv, nullptr, nullptr, Mn.pb2, nullptr, nullptr);
+            signal(4 + 3 * k, fo / (d / 4));
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc(tmem, 32);
+}
+
+// ---------------------------------------------------------------------------------------- host
+int task_stream_smem() { return ST_SMEM; }
+int task_stream_counter_bytes(int L) { return (3 * L + 3) * 5 * CNT_STRIDE * 4; }
+
+static bool stream_attr() {
+  static int done = 0;
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(task_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM);
+    if (e != cudaSuccess) {
+      set_error("task_stream smem attribute: %s", cudaGetErrorString(e));
+      return false;
+    }
+    e = cudaFuncSetAttribute(task_stream_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    done = 1;
+  }
+  return true;
+}
+
+static void stream_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, int clusters, cudaStream_t st) {
+  cfg = cudaLaunchConfig_t{};
+  cfg.gridDim = dim3(clusters * SK, 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = ST_SMEM;
+  cfg.stream = st;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = SK;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+}
+
+int task_stream_max_clusters(int dev) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(dev);
+  int n = 0;
+  if (stream_attr()) {
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute at[1];
+    stream_cfg(cfg, at, 1, nullptr);
+    if (cudaOccupancyMaxActiveClusters(&n, task_stream_kernel, &cfg) != cudaSuccess) n = 0;
+  }
+  cudaGetLastError();
+  cudaSetDevice(cur);
+  return n;
+}
+
+int task_stream_launch(cudaStream_t st, const STask& t, int clusters) {
+  if (!stream_attr()) return -3;
+  cudaError_t e = cudaMemsetAsync(t.cnt, 0, (size_t)task_stream_counter_bytes(t.L), st);
+  if (e != cudaSuccess) {
+    set_error("task_stream counter reset: %s", cudaGetErrorString(e));
+    return -3;
+  }
+  cudaLaunchConfig_t cfg;
+  cudaLaunchAttribute at[1];
+  stream_cfg(cfg, at, clusters, st);
+  e = cudaLaunchKernelEx(&cfg, task_stream_kernel, t);
+  if (e != cudaSuccess) {
+    set_error("task_stream launch (%d clusters): %s", clusters, cudaGetErrorString(e));
+    return -3;
+  }
+  return 0;
+}
+
+}  // namespace tgp

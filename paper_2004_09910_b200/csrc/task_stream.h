@@ -1,0 +1,62 @@
+// Persistent weight-streaming task kernel (task_stream.cu): device descriptors and host entry points.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tgp {
+
+// One pre-LN residual MLP block of a partition (micro-batch independent).
+struct alignas(64) SLayer {
+  CUtensorMap w1k;   // W1 [H][d] bf16, K-major box {64, 128}  (forward GEMM1: out H, K d)
+  CUtensorMap w2k;   // W2 [d][H] bf16, K-major box {64, 128}  (forward GEMM2: out d, K H)
+  CUtensorMap w2m;   // W2 [d][H] bf16, MN-major box {64, 64}  (backward dG = dY W2: out H, K d)
+  CUtensorMap w1m;   // W1 [H][d] bf16, MN-major box {64, 64}  (backward dH = dA W1: out d, K H)
+  CUtensorMap hop;   // Hop  [max_batch][d] bf16, box {64, 16}  (LN output = GEMM1 operand, dW1 stash)
+  CUtensorMap gop;   // Gop  [max_batch][H] bf16, box {64, 16}  (activation = GEMM2 operand, dW2 stash)
+  CUtensorMap dyop;  // dYop [max_batch][d] bf16, box {64, 16}  (output grad = dG operand, dW2 stash)
+  CUtensorMap daop;  // dAop [max_batch][H] bf16, box {64, 16}  (pre-act grad = dH operand, dW1 stash)
+  const float* gamma;
+  const float* beta;
+  const float* b1;
+  const float* b2;
+  uint32_t drop_thresh;  // dropout after GELU: keep iff (philox word >> 8) >= thresh (0 = none)
+  float drop_scale;
+  uint32_t site;         // global layer index (Philox counter word 2)
+  uint32_t pad;
+};
+
+// Per (micro-batch, block) pointers, pre-offset to the micro-batch's first row.
+struct SMicro {
+  const float* x;  // block input rows [M][d] fp32
+  float* y;        // block output rows [M][d] fp32
+  float* a;        // pre-activation [M][H] fp32 (written by F, read by B)
+  float* mean;     // LN statistics [M] (written by F, read by B)
+  float* rstd;
+  __nv_bfloat16 *hop, *gop, *dyop, *daop;  // operand stash rows (row r0)
+  float *pb, *pb2, *pg, *pbt;              // column-partial rows of this micro-batch: db1 [H], db2 [d], dgamma, dbeta [d]
+};
+
+struct STask {
+  const SLayer* layers;  // [L]
+  const SMicro* micro;   // [L], this micro-batch
+  int L, d, H, M, r0, bwd;
+  const float* gy_top;   // backward: incoming output gradient rows [M][d]
+  float* dx_bottom;      // backward: input gradient rows [M][d] (message source)
+  float* gbuf0;          // backward: inter-block gradient ping-pong [16][d]
+  float* gbuf1;
+  float* stats;          // [L + 1][d / 32][16][2] LN row statistics per 32-feature chunk
+  unsigned* cnt;         // dependency counters, one per 128-byte line: [(3L + 3) * 5]
+  uint64_t seed;
+  const uint32_t* step;  // device optimizer step (dropout counter word 3)
+};
+
+int task_stream_smem();
+int task_stream_counter_bytes(int L);
+// Clusters of 4 the device can co-schedule (0 if the kernel cannot run there).
+int task_stream_max_clusters(int dev);
+int task_stream_launch(cudaStream_t st, const STask& t, int clusters);
+
+}  // namespace tgp

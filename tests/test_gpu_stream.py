@@ -1,0 +1,83 @@
+"""GPU parity of the persistent weight-streaming task kernel (csrc/task_stream.cu): F, F' and B of
+all-RESMLP partitions with <= 16-row micro-batches run as ONE launch per task.  Compared with the
+fp64 oracle (normwise 2e-2, reading Z15) and with itself across checkpoint modes (F' == F bitwise,
+reading Z21).  Sizes span several 128-feature slabs per phase, d != H both ways, ragged
+micro-batches, dropout, two partitions on one device, and the full C2 block width."""
+import numpy as np
+import pytest
+
+from synth import configs as C
+
+from _gpu import compare, gpu_step, make_case, oracle_step
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _run(layers, B, m, n, ckpt, seed, options=None, balance=None):
+    x, t, params = make_case(layers, B, seed, "bf16")
+    g, P = gpu_step(layers, params, x, t, m=m, n=n, ckpt=ckpt, dtype="bf16", lr=0.05, seed=seed, balance=balance,
+                    options=options)
+    return x, t, params, g, P
+
+
+def _kernels_per_step(layers, B, m, stream):
+    x, t, params = make_case(layers, B, 1, "bf16")
+    g, P = gpu_step(layers, params, x, t, m=m, n=1, ckpt="except_last", dtype="bf16", lr=0.05, seed=1,
+                    options={"stream": stream})
+    P.close()
+    return g["kernels"]
+
+
+def test_stream_kernel_is_used():
+    layers = C.resmlp_stack(2, 512)
+    on, off = _kernels_per_step(layers, 64, 4, 1), _kernels_per_step(layers, 64, 4, 0)
+    # F, F', B are one counter reset + one kernel each with the stream kernel
+    assert on < off, (on, off)
+
+
+@pytest.mark.parametrize("d,H", [(1024, 2048), (1024, 512)])
+def test_stream_matches_oracle_and_is_bitwise_across_modes(d, H):
+    layers = C.resmlp_stack(3, d, hidden=H, dropout=0.1)
+    res = {}
+    for mode in ("always", "except_last", "never"):
+        x, t, params, g, P = _run(layers, 64, 4, 1, mode, 6)
+        res[mode] = g
+        P.close()
+    for mode in ("except_last", "never"):
+        assert res[mode]["loss"] == res["always"]["loss"]
+        for a, b in zip(res[mode]["grads"], res["always"]["grads"]):
+            assert np.array_equal(a, b)
+    ref = oracle_step(layers, params, x, t, lr=0.05, m=4, seed=6, step=0)
+    errs, bad = compare(res["never"], ref, params, TOL, 0.05)
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("B,m", [(60, 4), (50, 4), (16, 2)])
+def test_stream_ragged_micro_batches(B, m):
+    layers = C.resmlp_stack(2, 512, hidden=1024)
+    x, t, params, g, P = _run(layers, B, m, 1, "except_last", 11)
+    P.close()
+    ref = oracle_step(layers, params, x, t, lr=0.05, m=m, seed=11, step=0)
+    errs, bad = compare(g, ref, params, TOL, 0.05)
+    assert not bad, bad
+
+
+def test_stream_two_partitions_one_device():
+    layers = C.resmlp_stack(4, 512, dropout=0.1)
+    x, t, params, g, P = _run(layers, 64, 4, 2, "except_last", 4, balance=[2, 2])
+    P.close()
+    ref = oracle_step(layers, params, x, t, lr=0.05, m=4, seed=4, step=0)
+    errs, bad = compare(g, ref, params, TOL, 0.05)
+    assert not bad, bad
+
+
+def test_stream_full_c2_width_parity():
+    # the bench's launch configuration per block (d = H = 4096, 16-row micro-batches, m = 32) on 4 of
+    # C2's 32 blocks, so the fp64 oracle finishes in seconds
+    layers = C.resmlp_stack(4, 4096)
+    x, t, params, g, P = _run(layers, 512, 32, 1, "except_last", 1234)
+    P.close()
+    ref = oracle_step(layers, params, x, t, lr=0.05, m=32, seed=1234, step=0)
+    errs, bad = compare(g, ref, params, TOL, 0.05)
+    assert not bad, bad
