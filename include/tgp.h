@@ -177,12 +177,17 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *  "prefetch" L2 prefetch of the next GEMM's weights by the previous GEMM (default 0)
  *  "l2pf"     each weight-streaming GEMM prefetches its weight tiles beyond the shared-memory
  *             pipeline depth into L2 before its grid-dependency wait (default 0)
+ *  "stream"   run F / F' / B of all-RESMLP partitions with <= 16-row micro-batches as ONE persistent
+ *             weight-streaming kernel per task (task_stream.cu; default 1 where eligible)
  *  "persistent" run F / F' of all-RESMLP partitions (<= 16-row micro-batches) as ONE cooperative
  *             persistent kernel with grid barriers between phases (default 0)
  * Test-only negative controls (never used on the product path):
  *  "test_poison"        fill the forward receive slabs with NaN before each forward call
  *  "test_skip_wait"     drop the receive waits of partition `value` (-1 = none)
- *  "test_delay_push_us" delay every push on its copy stream by `value` microseconds */
+ *  "test_delay_push_us" delay every push on its copy stream by `value` microseconds
+ *  "test_stream_variant" timing experiments on the stream kernel (bit 0: ignore data dependencies,
+ *                       bit 1: contiguous weight tiles, bit 2: no L2 promotion, bit 3: evict-normal
+ *                       weights; bits 0 / 1 make the results garbage) */
 tgp_status tgp_set_option(tgp_ctx* ctx, const char* name, int64_t value);
 
 const char* tgp_last_error(void);
@@ -200,6 +205,13 @@ tgp_status tgp_bench_dominant_gemm(tgp_ctx* ctx, int32_t part, int32_t B, int32_
  * set): per CTA and grid-barrier id k < 256, the %globaltimer at its arrival and release, as
  * [grid][256][2] uint64.  out may be NULL to query *n. */
 tgp_status tgp_debug_pt_read(tgp_ctx* ctx, int32_t part, uint64_t* out, int64_t cap, int64_t* n);
+
+/* Diagnostics of the persistent weight-streaming task kernel (only when the process runs with
+ * TGP_ST_DEBUG set): per CTA and GEMM phase of the last task launched on partition `part`, 10
+ * %globaltimer stamps (B operand issued, first / last weight tile issued, B landed, last MMA, TMEM
+ * ready, partials received, outputs signalled, row statistics ready), as [grid][2L][10] uint64.
+ * out may be NULL to query *n. */
+tgp_status tgp_debug_stream_read(tgp_ctx* ctx, int32_t part, uint64_t* out, int64_t cap, int64_t* n);
 
 /* ------------------------------------------------------------------ kernel-level test entry */
 

@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ---------------------------------------------------------------------------------- host side
-bool make_map(CUtensorMap* map, const TcMat& t, int box_inner, int box_outer) {
+bool make_map(CUtensorMap* map, const TcMat& t, int box_inner, int box_outer, bool l2_promote) {
   const Driver* d = driver();
   if (!d) return false;
   cuuint64_t dims[2] = {(cuuint64_t)t.cols, (cuuint64_t)t.rows};
@@ -435,7 +435,8 @@ bool make_map(CUtensorMap* map, const TcMat& t, int box_inner, int box_outer) {
   cuuint32_t es[2] = {1, 1};
   CUresult r = d->tensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(t.ptr), dims,
                                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                       CU_TENSOR_MAP_SWIZZLE_128B,
+                                       l2_promote ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld box=%dx%d", (int)r,

@@ -23,7 +23,7 @@ struct TcMat {
 int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B0, const TcMat* B1, bool b_mn,
             GemmParams p, int splits);
 // 2-D bf16 TMA descriptor over a row-major matrix, 128-byte swizzle, box {box_inner, box_outer}.
-bool make_map(CUtensorMap* map, const TcMat& t, int box_inner, int box_outer);
+bool make_map(CUtensorMap* map, const TcMat& t, int box_inner, int box_outer, bool l2_promote = true);
 
 // fp32 SIMT GEMM with the same D = A * B^T semantics and epilogues, for fp32 mode (no TF32).
 // Operand element (i, k) of A is at A[i * a_si + k * a_sk]; of B at B[n * b_sn + k * b_sk]

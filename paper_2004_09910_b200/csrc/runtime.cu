@@ -310,8 +310,11 @@ static int st_build_desc(tgp_ctx* c, Stage& s, int B) {
     memset(&P, 0, sizeof(P));
     const void* w1 = wparam(c, s, Ly, 2);
     const void* w2 = wparam(c, s, Ly, 4);
-    if (!make_map(&P.w1k, TcMat{w1, H, d, d}, 64, 128) || !make_map(&P.w2k, TcMat{w2, d, H, H}, 64, 128) ||
-        !make_map(&P.w2m, TcMat{w2, d, H, H}, 64, 64) || !make_map(&P.w1m, TcMat{w1, H, d, d}, 64, 64) ||
+    const bool promo = !(c->st_flags & 4);  // test_stream_variant bit 2: no L2 256-byte promotion
+    if (!make_map(&P.w1k, TcMat{w1, H, d, d}, 64, 128, promo) || !make_map(&P.w2k, TcMat{w2, d, H, H}, 64, 128, promo) ||
+        !make_map(&P.w2m, TcMat{w2, d, H, H}, 64, 64, promo) || !make_map(&P.w1m, TcMat{w1, H, d, d}, 64, 64, promo) ||
+        !make_map(&P.w1c, TcMat{w1, (int64_t)H * d / 64, 64, 64}, 64, 128, promo) ||
+        !make_map(&P.w2c, TcMat{w2, (int64_t)H * d / 64, 64, 64}, 64, 128, promo) ||
         !make_map(&P.hop, TcMat{Ly.Hop, c->max_batch, d, d}, 64, 16) ||
         !make_map(&P.gop, TcMat{Ly.Gop, c->max_batch, H, H}, 64, 16) ||
         !make_map(&P.dyop, TcMat{Ly.dYop, c->max_batch, d, d}, 64, 16) ||
@@ -378,6 +381,15 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
   t.cnt = s.st_cnt;
   t.seed = c->seed;
   t.step = s.dstep;
+  t.flags = c->st_flags;
+  if (getenv("TGP_ST_DEBUG")) {  // diagnostics: per-CTA, per-phase %globaltimer stamps
+    const size_t nd = (size_t)s.st_clusters * 4 * 2 * t.L * ST_DBG_SLOTS;
+    if (!s.st_dbg) {
+      TGP_CUDA_TRY(cudaMalloc(&s.st_dbg, nd * 8));
+      TGP_CUDA_TRY(cudaMemset(s.st_dbg, 0, nd * 8));
+    }
+    t.dbg = s.st_dbg;
+  }
   c->kernels += 2;  // counter reset + task kernel
   return task_stream_launch(s.comp, t, s.st_clusters);
 }

@@ -109,6 +109,7 @@ struct Stage {
   int st_micro_B = -1;
   float* st_stats = nullptr;
   unsigned* st_cnt = nullptr;
+  unsigned long long* st_dbg = nullptr;  // diagnostics (TGP_ST_DEBUG): [grid][2L][ST_DBG_SLOTS]
   std::vector<TaskGraph> gF, gB;
   TaskGraph gW;
   bool grads_fresh = true;
@@ -146,7 +147,8 @@ struct tgp_ctx {
   // five ~2 us grid barriers per block dominate -- profiles/pt_phases.py)
   bool use_graphs = true, use_pdl = true, trace = false, poison = false, prefetch = false, persistent = false;
   bool l2pf = false;
-  bool stream = true;  // persistent weight-streaming task kernel where eligible (task_stream.cu)
+  bool stream = true;
+  int st_flags = 0;  // test only: bit 0 = stream kernel ignores dependencies (timing of the bare weight stream)  // persistent weight-streaming task kernel where eligible (task_stream.cu)
   int splitk = 0, skip_wait_part = -1;
   uint64_t delay_push_ns = 0;
   bool can_flush = false;

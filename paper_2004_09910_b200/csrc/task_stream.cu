@@ -7,8 +7,10 @@
 // intensity 15.9 FLOP/B): the task is a chain of 2 dependent 32 MiB weight reads
 // per block.  As separate kernels, every boundary drains and refills the HBM pipe.  Here the weight
 // stream of every CTA is static and independent of the activations, so it runs ahead continuously
-// across all GEMMs of the task through a 10-stage TMA ring; only the tiny activation operand of a
-// GEMM waits for its producers.
+// across all GEMMs of the task through an 11-stage TMA ring; only the tiny activation operand of a
+// GEMM waits for its producers: each ring stage holds a weight tile and the activation tile of the
+// same k-block, the latter loaded as soon as the phase's dependency is met (for tiles already in
+// the ring: then; for later tiles: together with the weight tile).
 //
 // Work split (grid = C clusters x 4 CTAs, one CTA per SM, C = max(d, H) / 128 <= 37):
 //  * every GEMM phase has out-features F (H or d) in 128-row slabs; cluster c owns slab c, its 4
@@ -43,13 +45,12 @@ namespace tgp {
 
 namespace {
 constexpr int SK = 4;                       // split-K ranks per cluster
-constexpr int ST_A = 16384;                 // 128 x 64 bf16 weight tile (one ring stage)
-constexpr int ST_B = 2048;                  // 16 x 64 bf16 activation tile
-constexpr int ST_STAGES = 10;               // weight ring depth
-constexpr int ST_BT = 16;                   // max k-blocks per rank per phase (K <= 4096)
+constexpr int ST_A = 16384;                 // 128 x 64 bf16 weight tile
+constexpr int ST_B = 2048;                  // 16 x 64 bf16 activation tile of the same k-block
+constexpr int ST_STAGE = ST_A + ST_B;       // one ring stage (both 1024-byte aligned)
+constexpr int ST_STAGES = 11;               // ring depth
 constexpr int ST_RECV = SK * 32 * 16 * 4;   // owner receive buffer: [src][32 features][16 rows] fp32
-constexpr int OFF_B = ST_STAGES * ST_A;
-constexpr int OFF_RECV = OFF_B + ST_BT * ST_B;
+constexpr int OFF_RECV = ST_STAGES * ST_STAGE;
 constexpr int OFF_BAR = OFF_RECV + 2 * ST_RECV;
 constexpr int ST_SMEM = OFF_BAR + 2048 + 1024;
 constexpr int CNT_STRIDE = 32;              // uints between counters (one 128-byte line each)
@@ -60,7 +61,18 @@ TGP_DEV unsigned ld_relaxed_u32(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+TGP_DEV uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 TGP_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+TGP_DEV void dbg_stamp(const STask& t, int p, int slot) {
+  if (!t.dbg) return;
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  t.dbg[((size_t)blockIdx.x * 2 * t.L + p) * ST_DBG_SLOTS + slot] = v;
+}
 
 template <typename T>
 TGP_DEV T wsum32(T v) {
@@ -87,15 +99,12 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
-  uint8_t* bbuf = smem + OFF_B;
   float* recv = reinterpret_cast<float*>(smem + OFF_RECV);  // [2][SK][32][16]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* empty = full + ST_STAGES;
   uint64_t* tfull = empty + ST_STAGES;  // [2] TMEM accumulator ready
   uint64_t* tempty = tfull + 2;         // [2] TMEM accumulator drained (128 arrivals)
-  uint64_t* bfull = tempty + 2;         // activation tiles of a phase landed
-  uint64_t* bempty = bfull + 1;         // MMAs of a phase done (activation buffer reusable)
-  uint64_t* rbar = bempty + 1;          // [2] split-K partials of a phase received (owner)
+  uint64_t* rbar = tempty + 2;          // [2] split-K partials of a phase received (owner)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
   float* rmu = reinterpret_cast<float*>(smem + OFF_BAR + 512);  // [16] row statistics
   float* rrs = rmu + 16;                                        // [16]
@@ -119,8 +128,6 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
       mbar_init(&tempty[b], 128);
       mbar_init(&rbar[b], 1);
     }
-    mbar_init(bfull, 1);
-    mbar_init(bempty, 1);
     fence_barrier_init();
     // first use of each receive buffer: 4 sources x 32 features x 16 rows x 4 B
     mbar_arrive_expect_tx(&rbar[0], ST_RECV);
@@ -136,23 +143,47 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
   if (warp == 0) {
     if (elect_one()) {
       // ------------------------------------------------------------ TMA producer
-      const uint64_t pol_w = policy_evict_first(), pol_b = policy_evict_last();
+      const uint64_t pol_w = (t.flags & 8) ? policy_evict_normal() : policy_evict_first(), pol_b = policy_evict_last();
       auto next_active = [&](int p) {
         while (p < NP && !active(p)) ++p;
         return p;
       };
       int wp = next_active(0), wkb = 0, it = 0;  // weight cursor: phase, k-block, ring tile
-      int bp = next_active(0), nb = 0;           // next phase whose activation tiles to load
-      while (wp < NP || bp < NP) {
+      int rp = next_active(0), rt0 = 0;          // lowest phase whose activations are not released; its first tile
+      auto load_b = [&](int p, int kb, int tile) {
+        const Ph P = phase_of(t, p);
+        const int nkb = P.K / (SK * 64);
+        const int s = tile % ST_STAGES;
+        tma_load_2d(P.B, &full[s], ring + s * ST_STAGE + ST_A, (rank * nkb + kb) * 64, t.r0, pol_b);
+      };
+      // optional L2 prefetch of the weight tiles `pfd` tiles ahead of the ring (test_stream_variant
+      // bits 4-9; measured: any distance makes the task slower -- profiles/r1o_st_variants.txt)
+      const int pfd = (t.flags >> 4) & 63;
+      int pq = wp, pkb = 0;
+      auto prefetch_next = [&]() {
+        if (pq >= NP) return;
+        const Ph P = phase_of(t, pq);
+        const int nkb = P.K / (SK * 64);
+        const int kc = (rank * nkb + pkb) * 64;
+        if (!t.bwd) {
+          tma_prefetch_l2_2d(P.A, kc, slab * 128);
+        } else {
+          tma_prefetch_l2_2d(P.A, slab * 128, kc);
+          tma_prefetch_l2_2d(P.A, slab * 128 + 64, kc);
+        }
+        if (++pkb == nkb) {
+          pkb = 0;
+          pq = next_active(pq + 1);
+        }
+      };
+      for (int q = 0; q < ST_STAGES + pfd && pfd > 0; ++q) prefetch_next();
+      while (wp < NP || rp < NP) {
         bool progress = false;
-        // poll the dependency of the next activation load (issued first, used after the weight loop)
+        // poll the dependency of phase rp (issued first, used after the weight loop)
         unsigned have = 0, need = 0;
-        const unsigned* dep = nullptr;
-        const bool b_free = bp < NP && (nb == 0 || mbar_test_wait(smem_u32(bempty), (uint32_t)((nb - 1) & 1)));
-        if (b_free) {
-          dep = cnt(1 + 3 * (bp >> 1) + (bp & 1), rank);
-          need = (unsigned)(phase_of(t, bp).K / 128);
-          have = ld_relaxed_u32(dep);
+        if (rp < NP) {
+          need = (unsigned)(phase_of(t, rp).K / 128);
+          have = (t.flags & 1) ? need : ld_relaxed_u32(cnt(1 + 3 * (rp >> 1) + (rp & 1), rank));
         }
         while (wp < NP) {  // weights: run ahead as far as the ring allows
           const int s = it % ST_STAGES, r = it / ST_STAGES;
@@ -160,13 +191,23 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           const Ph P = phase_of(t, wp);
           const int nkb = P.K / (SK * 64);
           const int kc = (rank * nkb + wkb) * 64;
-          mbar_arrive_expect_tx(&full[s], ST_A);
-          if (!t.bwd) {
-            tma_load_2d(P.A, &full[s], ring + s * ST_A, kc, slab * 128, pol_w);
+          if (wkb == 0) dbg_stamp(t, wp, 1);
+          if (wkb == nkb - 1) dbg_stamp(t, wp, 2);
+          uint8_t* dst = ring + s * ST_STAGE;
+          mbar_arrive_expect_tx(&full[s], ST_STAGE);
+          if (t.flags & 2) {
+            const SLayer& Ly = t.layers[t.bwd ? t.L - 1 - (wp >> 1) : (wp >> 1)];
+            const CUtensorMap* cm = ((wp & 1) != t.bwd) ? &Ly.w2c : &Ly.w1c;
+            const int tile = slab * (P.K / 64) + rank * nkb + wkb;
+            tma_load_2d(cm, &full[s], dst, 0, tile * 128, pol_w);
+          } else if (!t.bwd) {
+            tma_load_2d(P.A, &full[s], dst, kc, slab * 128, pol_w);
           } else {
-            tma_load_2d(P.A, &full[s], ring + s * ST_A, slab * 128, kc, pol_w);
-            tma_load_2d(P.A, &full[s], ring + s * ST_A + 8192, slab * 128 + 64, kc, pol_w);
+            tma_load_2d(P.A, &full[s], dst, slab * 128, kc, pol_w);
+            tma_load_2d(P.A, &full[s], dst + 8192, slab * 128 + 64, kc, pol_w);
           }
+          if (wp < rp) load_b(wp, wkb, it);  // this phase's activations are already released
+          if (pfd > 0) prefetch_next();
           ++it;
           progress = true;
           if (++wkb == nkb) {
@@ -174,15 +215,15 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             wp = next_active(wp + 1);
           }
         }
-        if (dep && have >= need) {
+        if (rp < NP && have >= need) {
+          // release phase rp: activation tiles for its k-blocks already in the ring
           fence_acq_rel_gpu();
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          const Ph P = phase_of(t, bp);
-          const int nkb = P.K / (SK * 64);
-          mbar_arrive_expect_tx(bfull, (uint32_t)(nkb * ST_B));
-          for (int q = 0; q < nkb; ++q) tma_load_2d(P.B, bfull, bbuf + q * ST_B, (rank * nkb + q) * 64, t.r0, pol_b);
-          ++nb;
-          bp = next_active(bp + 1);
+          dbg_stamp(t, rp, 0);
+          const int nkb = phase_of(t, rp).K / (SK * 64);
+          for (int q = rt0; q < it && q < rt0 + nkb; ++q) load_b(rp, q - rt0, q);
+          rt0 += nkb;
+          rp = next_active(rp + 1);
           progress = true;
         }
         if (!progress) __nanosleep(32);
@@ -205,11 +246,8 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           const int s = it % ST_STAGES, r = it / ST_STAGES;
           mbar_wait(&full[s], (uint32_t)(r & 1));
           tc_fence_after();
-          if (kb == 0) {
-            mbar_wait(bfull, (uint32_t)(n & 1));
-            tc_fence_after();
-          }
-          const uint32_t a = smem_u32(ring + s * ST_A), b = smem_u32(bbuf + kb * ST_B);
+          if (kb == 0) dbg_stamp(t, p, 3);
+          const uint32_t a = smem_u32(ring + s * ST_STAGE), b = a + ST_A;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint64_t ad = t.bwd ? make_sdesc_sw128(a + kk * 2048, 8192, 1024) : make_sdesc_sw128(a + kk * 32, 16, 1024);
@@ -217,8 +255,8 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           }
           tc_commit(&empty[s]);
         }
+        dbg_stamp(t, p, 4);
         tc_commit(&tfull[buf]);
-        tc_commit(bempty);
         ++n;
       }
     }
@@ -229,19 +267,21 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
     const int et = threadIdx.x - 64, ew = et >> 5, lg = warp & 3;
     const int fo = slab * 128 + rank * 32 + lane;
     const int chunk = slab * SK + rank;  // 32-feature chunk index of the owner slice
-    int n = 0;
+    int n = 0, cur_p = 0;
     auto epi_bar = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
     auto signal = [&](int id, int q) {
       epi_bar();
       if (et == 0) {
-        __threadfence();
-        atomicAdd(cnt(id, q), 1u);
+        // release: the epilogue barrier orders the other threads' stores before this reduction
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(cnt(id, q)), "r"(1u) : "memory");
+        dbg_stamp(t, cur_p, 7);
       }
     };
     auto wait_cnt = [&](int id, int q, unsigned need) {
       if (et == 0) {
-        while (ld_relaxed_u32(cnt(id, q)) < need) __nanosleep(32);
+        while (!(t.flags & 1) && ld_relaxed_u32(cnt(id, q)) < need) __nanosleep(32);
         fence_acq_rel_gpu();
+        dbg_stamp(t, cur_p, 8);
       }
       epi_bar();
     };
@@ -269,6 +309,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
       const int buf = n & 1, u = n >> 1;
       mbar_wait(&tfull[buf], (uint32_t)(u & 1));
       tc_fence_after();
+      if (et == 0) dbg_stamp(t, cur_p, 5);
       float v[16];
       tmem_ld16(tmem + (uint32_t)(buf * 16) + ((uint32_t)(lg * 32) << 16), v);
       tc_fence_before();
@@ -282,6 +323,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
                        make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]), dbar);
       }
       mbar_wait(&rbar[buf], (uint32_t)(u & 1));
+      if (et == 0) dbg_stamp(t, cur_p, 6);
       const float4* r4 = reinterpret_cast<const float4*>(recv + buf * (ST_RECV / 4));
       float4 a = r4[(0 * 32 + lane) * 4 + (ew ^ (lane & 3))];
 #pragma unroll
@@ -378,6 +420,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
       for (int l = 0; l < t.L; ++l) {
         const SLayer& Ly = t.layers[l];
         const SMicro& Mi = t.micro[l];
+        cur_p = 2 * l;
         if (own_h) {  // GEMM1 epilogue: a = acc + b1; g = dropout(GELU(a))
           const float b1 = Ly.b1[fo];
           const uint32_t step = Ly.drop_thresh ? *t.step : 0u;
@@ -388,7 +431,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             const int r = 4 * ew + e;
             if (r >= M) continue;
             const float z = acc[e] + b1;
-            Mi.a[(size_t)r * H + fo] = z;
+            acc[e] = z;
             float gv = gelu_f(z);
             if (Ly.drop_thresh) {
               const uint64_t idx = (uint64_t)(t.r0 + r) * (uint64_t)H + (uint64_t)fo;
@@ -397,7 +440,12 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             Mi.gop[(size_t)r * H + fo] = __float2bfloat16_rn(gv);
           }
           signal(2 + 3 * l, fo / (H / 4));
+          // the pre-activation is only read by the backward task: stored off the critical path
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * ew + e < M) Mi.a[(size_t)(4 * ew + e) * H + fo] = acc[e];
         }
+        cur_p = 2 * l + 1;
         if (own_d) {  // GEMM2 epilogue: y = x + acc + b2, then LN of the next block
           const float b2 = Ly.b2[fo];
           float xr[4];
@@ -412,9 +460,12 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           for (int e = 0; e < 4; ++e) {
             const int r = 4 * ew + e;
             y[e] = r < M ? acc[e] + b2 + xr[e] : 0.0f;
-            if (r < M) Mi.y[(size_t)r * d + fo] = y[e];
           }
           if (l + 1 < t.L) layernorm(y, l + 1, 3 + 3 * l, 4 + 3 * l);
+          // the residual stream is read by this thread (next block) and later tasks only
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * ew + e < M) Mi.y[(size_t)(4 * ew + e) * d + fo] = y[e];
         }
       }
     } else {
@@ -436,6 +487,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
         const int l = L - 1 - k;
         const SLayer& Ly = t.layers[l];
         const SMicro& Mi = t.micro[l];
+        cur_p = 2 * k;
         if (own_h) {  // dG epilogue: dA = dG * dropout mask * GELU'(a)
           const uint32_t step = Ly.drop_thresh ? *t.step : 0u;
           float av[4];
@@ -459,9 +511,10 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             da[e] = dg * gelu_df(av[e]);
             Mi.daop[(size_t)r * H + fo] = __float2bfloat16_rn(da[e]);
           }
-          colsums(da, nullptr, nullptr, Mi.pb, nullptr, nullptr);
           signal(2 + 3 * k, fo / (H / 4));
+          colsums(da, nullptr, nullptr, Mi.pb, nullptr, nullptr);
         }
+        cur_p = 2 * k + 1;
         if (own_d) {  // dH epilogue: LayerNorm backward + residual
           const float gam = Ly.gamma[fo];
           const float* gy = (l == L - 1) ? t.gy_top : (((l + 1) & 1) ? t.gbuf1 : t.gbuf0);
@@ -522,18 +575,20 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             dxv[e] = 0.0f;
             if (r >= M) continue;
             dxv[e] = gyv[e] + rsv[e] * (dn[e] - rmu[r] - nv[e] * rrs[r]);
-            dx[(size_t)r * d + fo] = dxv[e];
           }
-          if (l > 0) {
+          if (l > 0) {  // the next block's dG operand first (critical path), then the rest
             const SMicro& Mn = t.micro[l - 1];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int r = 4 * ew + e;
               if (r < M) Mn.dyop[(size_t)r * d + fo] = __float2bfloat16_rn(dxv[e]);
             }
-            colsums(dxv, nullptr, nullptr, Mn.pb2, nullptr, nullptr);
             signal(4 + 3 * k, fo / (d / 4));
+            colsums(dxv, nullptr, nullptr, Mn.pb2, nullptr, nullptr);
           }
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * ew + e < M) dx[(size_t)(4 * ew + e) * d + fo] = dxv[e];
         }
       }
     }

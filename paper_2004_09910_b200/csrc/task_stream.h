@@ -18,6 +18,8 @@ struct alignas(64) SLayer {
   CUtensorMap gop;   // Gop  [max_batch][H] bf16, box {64, 16}  (activation = GEMM2 operand, dW2 stash)
   CUtensorMap dyop;  // dYop [max_batch][d] bf16, box {64, 16}  (output grad = dG operand, dW2 stash)
   CUtensorMap daop;  // dAop [max_batch][H] bf16, box {64, 16}  (pre-act grad = dH operand, dW1 stash)
+  CUtensorMap w1c;   // diagnostics: W1 viewed as contiguous 16 KB tiles [H*d/64][64], box {64, 128}
+  CUtensorMap w2c;   // diagnostics: W2 likewise
   const float* gamma;
   const float* beta;
   const float* b1;
@@ -51,7 +53,15 @@ struct STask {
   unsigned* cnt;         // dependency counters, one per 128-byte line: [(3L + 3) * 5]
   uint64_t seed;
   const uint32_t* step;  // device optimizer step (dropout counter word 3)
+  // diagnostics only (nullptr / 0 on the product path): per CTA and phase, %globaltimer stamps
+  // [grid][2L][ST_DBG_SLOTS]; flags (test_stream_variant): bit 0 = ignore dependencies, bit 1 = read
+  // each weight tile as one contiguous 16 KB block, bit 2 = no L2 promotion (host), bit 3 =
+  // evict-normal weight policy, bits 4-9 = L2 prefetch distance in tiles (timing experiments:
+  // bits 0/1 make the results garbage)
+  unsigned long long* dbg;
+  int flags;
 };
+constexpr int ST_DBG_SLOTS = 10;
 
 int task_stream_smem();
 int task_stream_counter_bytes(int L);
