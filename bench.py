@@ -231,7 +231,12 @@ def run_tgp(args):
     e2e_ms, _, _ = timed(args.steps, True)
 
     # dominant kernel: forward weight-streaming GEMM, timed live on its stream (cycling cold weights)
-    gemm_ms, gemm_bytes, gemm_n = P.bench_dominant_gemm(rank, BATCH, reps=3)
+    # dominant kernel: the persistent weight-streaming task kernel (F task of micro-batch 1: 2 GEMMs
+    # per block, weights streamed from HBM), timed live on the partition's compute stream
+    stream = P.stream_enabled(rank)
+    gemm_ms, gemm_bytes, gemm_n = P.bench_dominant_gemm(rank, BATCH, reps=10 if stream else 3)
+    kname = (f"task_stream_kernel F task ({BLOCKS // n} blocks x 2 weight-streaming GEMMs, M=16 rows, d=H={WIDTH})"
+             if stream else "gemm_tc_kernel<16> forward W1 GEMM (M=16 rows, K=N=4096)")
     peaks = _peaks()
     if peaks and "hbm_gbs" in peaks:
         peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
@@ -253,7 +258,7 @@ def run_tgp(args):
                     "h2d_bytes_per_step": 4 * BATCH * WIDTH * 2, "d2h_bytes_per_step": 8},
             "gpu_launches": int(nk),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": "gemm_tc_kernel<16> forward W1 GEMM (M=16 rows, K=N=4096)",
+                         "traffic": None, "kernel": kname,
                          "algorithmic_bytes_per_launch": gemm_bytes, "avg_launch_us": gemm_ms * 1e3,
                          "launches_timed": gemm_n, "peak_source": peak_src},
             "clocks": clocks,

@@ -201,6 +201,12 @@ const char* tgp_last_error(void);
 tgp_status tgp_bench_dominant_gemm(tgp_ctx* ctx, int32_t part, int32_t B, int32_t reps, double* ms, double* bytes,
                                    int64_t* launches);
 
+/* *on = 1 iff local partition `part` runs its F / F' / B tasks as the persistent weight-streaming
+ * task kernel (eligible shape and option "stream" on); then tgp_bench_dominant_gemm times that
+ * kernel (F_{1,j} launches: *bytes = its algorithmic bytes -- weights plus activations read and
+ * written once) instead of the per-layer forward GEMM. */
+tgp_status tgp_stream_enabled(tgp_ctx* ctx, int32_t part, int32_t* on);
+
 /* Diagnostics of the persistent forward-task kernel (only when the process runs with TGP_PT_DEBUG
  * set): per CTA and grid-barrier id k < 256, the %globaltimer at its arrival and release, as
  * [grid][256][2] uint64.  out may be NULL to query *n. */

@@ -68,6 +68,7 @@ _SIGS = {
                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)],
     "tgp_debug_pt_read": [_P, _I32, _P, _I64, ctypes.POINTER(_I64)],
     "tgp_debug_stream_read": [_P, _I32, _P, _I64, ctypes.POINTER(_I64)],
+    "tgp_stream_enabled": [_P, _I32, ctypes.POINTER(_I32)],
     "tgp_test_gemm_bf16": [_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P],
 }
 
@@ -280,6 +281,11 @@ class Pipeline:
         _check(lib().tgp_bench_dominant_gemm(self.h, part, B, reps, ctypes.byref(ms), ctypes.byref(by),
                                              ctypes.byref(n)), "tgp_bench_dominant_gemm")
         return ms.value, by.value, n.value
+
+    def stream_enabled(self, part):
+        on = _I32()
+        _check(lib().tgp_stream_enabled(self.h, part, ctypes.byref(on)), "tgp_stream_enabled")
+        return bool(on.value)
 
     def set_option(self, name, value):
         _check(lib().tgp_set_option(self.h, name.encode(), int(value)), "tgp_set_option")

@@ -30,7 +30,14 @@ def _kernels_per_step(layers, B, m, stream):
 
 
 def test_stream_kernel_is_used():
+    from paper_2004_09910_b200 import Pipeline
+
     layers = C.resmlp_stack(2, 512)
+    P = Pipeline(layers, chunks=4, devices=[0], checkpoint="except_last", max_batch=64, dtype="bf16")
+    assert P.stream_enabled(0)
+    P.set_option("stream", 0)
+    assert not P.stream_enabled(0)
+    P.close()
     on, off = _kernels_per_step(layers, 64, 4, 1), _kernels_per_step(layers, 64, 4, 0)
     # F, F', B are one counter reset + one kernel each with the stream kernel
     assert on < off, (on, off)
