@@ -320,10 +320,14 @@ static int st_build_desc(tgp_ctx* c, Stage& s, int B) {
         !make_map(&P.dyop, TcMat{Ly.dYop, c->max_batch, d, d}, 64, 16) ||
         !make_map(&P.daop, TcMat{Ly.dAop, c->max_batch, H, H}, 64, 16))
       return TGP_E_CUDA;
+    if (!make_map(&P.ygm, TcMat{s.st_yg, 16, d, d}, 64, 16)) return TGP_E_CUDA;
     P.gamma = mparam(s, Ly, 0);
     P.beta = mparam(s, Ly, 1);
     P.b1 = mparam(s, Ly, 3);
     P.b2 = mparam(s, Ly, 5);
+    P.cfold = s.st_fold + (size_t)(l - s.l0) * 2 * H;
+    P.efold = P.cfold + H;
+    P.yg = (__nv_bfloat16*)s.st_yg;
     P.drop_thresh = drop_thresh(Ly.L.dropout);
     P.drop_scale = Ly.L.dropout > 0 ? 1.0f / (1.0f - Ly.L.dropout) : 1.0f;
     P.site = (uint32_t)l;
@@ -361,6 +365,22 @@ static int st_build_desc(tgp_ctx* c, Stage& s, int B) {
 }
 
 static bool use_stream(const tgp_ctx* c, const Stage& s, int M) { return s.st_ok && c->stream && M <= 16; }
+
+// LayerNorm folded into GEMM1 of the stream kernel: recompute c = W1 gamma, e = W1 beta + b1 of
+// every block after the weights or LN parameters changed (SGD step, set / init).
+static int st_refold(tgp_ctx* c, Stage& s) {
+  if (!s.st_ok || !s.fold_dirty) return 0;
+  for (int l = s.l0; l < s.l1; ++l) {
+    LayerRT& Ly = c->layers[l];
+    const int d = Ly.L.d_in, H = Ly.L.d_hidden;
+    float* cf = s.st_fold + (size_t)(l - s.l0) * 2 * H;
+    TGP_TRY(task_stream_fold(s.comp, (const __nv_bfloat16*)wparam(c, s, Ly, 2), d, H, mparam(s, Ly, 0),
+                             mparam(s, Ly, 1), mparam(s, Ly, 3), cf, cf + H));
+    c->kernels++;
+  }
+  s.fold_dirty = false;
+  return 0;
+}
 
 static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd) {
   const LayerRT& L0 = c->layers[s.l0];

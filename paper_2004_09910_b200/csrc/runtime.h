@@ -109,6 +109,9 @@ struct Stage {
   int st_micro_B = -1;
   float* st_stats = nullptr;
   unsigned* st_cnt = nullptr;
+  float* st_fold = nullptr;   // per block [2][H]: LN folded into GEMM1 (c = W1 gamma, e = W1 beta + b1)
+  void* st_yg = nullptr;      // [16][d] bf16: GEMM1 operand gamma (y - mu~) of the current block
+  bool fold_dirty = true;     // weights / LN parameters changed since st_fold was computed
   unsigned long long* st_dbg = nullptr;  // diagnostics (TGP_ST_DEBUG): [grid][2L][ST_DBG_SLOTS]
   std::vector<TaskGraph> gF, gB;
   TaskGraph gW;

@@ -26,9 +26,11 @@
 //    go through per-32-feature chunk statistics and one global counter, combined in fixed order.
 //
 // Phases.  Forward, block l (ids are dependency counters):
-//   [l = 0] LN(x) statistics (id 0) -> h_0 = LN(x) bf16 (id 1)
-//   GEMM1 a = h W1^T + b1 -> g = dropout(GELU(a)) bf16        (id 2 + 3l)
-//   GEMM2 y = x + g W2^T + b2 -> [l < L-1] stats (id 3 + 3l) -> h_{l+1} = LN(y) (id 4 + 3l)
+//   input y of block l (x for l = 0): operand gamma (y - mu~) bf16 (id 1 + 3l, quarters) and LN
+//                                     chunk statistics (id 3 + 3l, global)
+//   GEMM1 a = LN(y) W1^T + b1, LayerNorm folded (see ln_produce) -> g = dropout(GELU(a)) bf16
+//                                                                   (id 2 + 3l)
+//   GEMM2 y' = y + g W2^T + b2 -> the next block's operand and statistics (ids 4 + 3l, 6 + 3l)
 // Backward, k = 0..L-1 over blocks l = L-1-k:
 //   [k = 0] dY_top bf16 + db2 column sums (id 1)
 //   dG = dY W2 -> dA = dG * dropout' * GELU'(a) bf16, db1 column sums       (id 2 + 3k)
@@ -52,7 +54,7 @@ constexpr int ST_STAGES = 11;               // ring depth
 constexpr int ST_RECV = SK * 32 * 16 * 4;   // owner receive buffer: [src][32 features][16 rows] fp32
 constexpr int OFF_RECV = ST_STAGES * ST_STAGE;
 constexpr int OFF_BAR = OFF_RECV + 2 * ST_RECV;
-constexpr int ST_SMEM = OFF_BAR + 2048 + 1024;
+constexpr int ST_SMEM = OFF_BAR + 3072 + 1024;
 constexpr int CNT_STRIDE = 32;              // uints between counters (one 128-byte line each)
 }  // namespace
 
@@ -91,7 +93,7 @@ TGP_DEV Ph phase_of(const STask& t, int p) {
   const int k = p >> 1, sub = p & 1;
   const int l = t.bwd ? t.L - 1 - k : k;
   const SLayer& Ly = t.layers[l];
-  if (!t.bwd) return sub ? Ph{&Ly.w2k, &Ly.gop, t.H, t.d} : Ph{&Ly.w1k, &Ly.hop, t.d, t.H};
+  if (!t.bwd) return sub ? Ph{&Ly.w2k, &Ly.gop, t.H, t.d} : Ph{&Ly.w1k, &Ly.ygm, t.d, t.H};
   return sub ? Ph{&Ly.w1m, &Ly.daop, t.H, t.d} : Ph{&Ly.w2m, &Ly.dyop, t.d, t.H};
 }
 
@@ -154,7 +156,9 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
         const Ph P = phase_of(t, p);
         const int nkb = P.K / (SK * 64);
         const int s = tile % ST_STAGES;
-        tma_load_2d(P.B, &full[s], ring + s * ST_STAGE + ST_A, (rank * nkb + kb) * 64, t.r0, pol_b);
+        // forward GEMM1 reads the [16][d] task scratch gamma (y - mu~) (row 0), all others the stash rows
+        const int row = (!t.bwd && !(p & 1)) ? 0 : t.r0;
+        tma_load_2d(P.B, &full[s], ring + s * ST_STAGE + ST_A, (rank * nkb + kb) * 64, row, pol_b);
       };
       // optional L2 prefetch of the weight tiles `pfd` tiles ahead of the ring (test_stream_variant
       // bits 4-9; measured: any distance makes the task slower -- profiles/r1o_st_variants.txt)
@@ -343,94 +347,120 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
       acc[3] = a.w;
       ++n;
     };
-    // forward LayerNorm of block `l` over d features from the owner values y[4] (rows 4ew..):
-    // chunk statistics (mean, M2) -> global counter id_st -> fixed-order combination (identical in
-    // every CTA) -> h = gamma (y - mu) rstd + beta (bf16), mean / rstd saved for the backward.
-    auto layernorm = [&](const float* y, int l, int id_st, int id_out) {
+    // Forward LayerNorm folded into GEMM1 (reading R3 in DESIGN.md).  With mu, rs the statistics
+    // of the block input y and mu~ the input mean of the previous block (0 for the first):
+    //   a = LN(y) W1^T + b1 = rs (sum_k bf16(gamma_k (y_k - mu~)) W1[h][k] - (mu - mu~) c_h) + e_h
+    // with c_h = sum_k gamma_k W1[h][k], e_h = sum_k beta_k W1[h][k] + b1[h] (task_stream_fold).  The
+    // GEMM1 operand needs no row statistics, so the statistics exchange overlaps GEMM1 instead of
+    // preceding it; the exact LN output (dW1 stash) and mean / rstd are written off the critical path.
+    //
+    // producer side (owners of the block input, d-space): chunk statistics (mean, M2 over the 32
+    // features) and the operand gamma (y - mu~), then the quarter counter (operand) and the global
+    // counter (statistics).  mut[e] = mu~ of row 4ew+e.
+    auto ln_produce = [&](const float* y, const float* mut, int l) {
       const SLayer& Ly = t.layers[l];
-      const SMicro& Mi = t.micro[l];
       const int J = d / 32;
       float* st = t.stats + (size_t)l * J * 32;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float mu = wsum32(y[e]) * (1.0f / 32.0f);
-        const float dv = y[e] - mu;
-        const float m2 = wsum32(dv * dv);
-        if (lane == 0) *reinterpret_cast<float2*>(st + ((size_t)chunk * 16 + 4 * ew + e) * 2) = make_float2(mu, m2);
-      }
-      const float g = Ly.gamma[fo], b = Ly.beta[fo];
-      signal(id_st, 4);
-      wait_cnt(id_st, 4, (unsigned)J);
-      {
-        const int rr = et >> 3, jl = et & 7;
-        float2 sv[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int j = jl + 8 * u;
-          sv[u] = j < J ? __ldcg(reinterpret_cast<const float2*>(st + ((size_t)j * 16 + rr) * 2)) : make_float2(0.f, 0.f);
-        }
-        float mu = 0.0f;
-#pragma unroll
-        for (int u = 0; u < 16; ++u) mu += sv[u].x;
-        mu += __shfl_xor_sync(0xffffffffu, mu, 4);
-        mu += __shfl_xor_sync(0xffffffffu, mu, 2);
-        mu += __shfl_xor_sync(0xffffffffu, mu, 1);
-        mu /= (float)J;
-        float m2 = 0.0f;
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (jl + 8 * u < J) {
-            const float dm = sv[u].x - mu;
-            m2 += sv[u].y + 32.0f * dm * dm;
-          }
-        m2 += __shfl_xor_sync(0xffffffffu, m2, 4);
-        m2 += __shfl_xor_sync(0xffffffffu, m2, 2);
-        m2 += __shfl_xor_sync(0xffffffffu, m2, 1);
-        const float rs = 1.0f / sqrtf(m2 / (float)d + 1e-5f);
-        if (jl == 0) {
-          rmu[rr] = mu;
-          rrs[rr] = rs;
-          if (blockIdx.x == 0 && rr < M) {
-            Mi.mean[rr] = mu;
-            Mi.rstd[rr] = rs;
-          }
-        }
-      }
-      epi_bar();
+      const float g = Ly.gamma[fo];
+      // the operand first (critical path: the next GEMM1's activation tiles), statistics after
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = 4 * ew + e;
-        if (r < M) Mi.hop[(size_t)r * d + fo] = __float2bfloat16_rn(g * ((y[e] - rmu[r]) * rrs[r]) + b);
+        Ly.yg[(size_t)r * d + fo] = __float2bfloat16_rn(r < M ? g * (y[e] - mut[e]) : 0.0f);
       }
-      signal(id_out, fo / (d / 4));
+      signal(1 + 3 * l, fo / (d / 4));
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = 4 * ew + e;
+        const float mu = wsum32(y[e]) * (1.0f / 32.0f);
+        const float dv = y[e] - mu;
+        const float m2 = wsum32(dv * dv);
+        if (lane == 0) *reinterpret_cast<float2*>(st + ((size_t)chunk * 16 + r) * 2) = make_float2(mu, m2);
+      }
+      signal(3 + 3 * l, 4);
+    };
+    // consumer side: wait for all chunk statistics of block l's input, combine them in fixed order
+    // (identical in every CTA) into rmu / rrs; the previous means move to rmp.
+    float* rmp = cs + 3 * 4 * 32;  // [16] mu~ of the current block (previous block's input mean)
+    auto ln_rows = [&](int l) {
+      const int J = d / 32;
+      const float* st = t.stats + (size_t)l * J * 32;
+      wait_cnt(3 + 3 * l, 4, (unsigned)J);
+      const int rr = et >> 3, jl = et & 7;
+      float2 sv[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int j = jl + 8 * u;
+        sv[u] = j < J ? __ldcg(reinterpret_cast<const float2*>(st + ((size_t)j * 16 + rr) * 2)) : make_float2(0.f, 0.f);
+      }
+      float mu = 0.0f;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) mu += sv[u].x;
+      mu += __shfl_xor_sync(0xffffffffu, mu, 4);
+      mu += __shfl_xor_sync(0xffffffffu, mu, 2);
+      mu += __shfl_xor_sync(0xffffffffu, mu, 1);
+      mu /= (float)J;
+      float m2 = 0.0f;
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (jl + 8 * u < J) {
+          const float dm = sv[u].x - mu;
+          m2 += sv[u].y + 32.0f * dm * dm;
+        }
+      m2 += __shfl_xor_sync(0xffffffffu, m2, 4);
+      m2 += __shfl_xor_sync(0xffffffffu, m2, 2);
+      m2 += __shfl_xor_sync(0xffffffffu, m2, 1);
+      const float rs = 1.0f / sqrtf(m2 / (float)d + 1e-5f);
+      if (jl == 0) {
+        rmp[rr] = l == 0 ? 0.0f : rmu[rr];
+        rmu[rr] = mu;
+        rrs[rr] = rs;
+        if (blockIdx.x == 0 && rr < M) {
+          t.micro[l].mean[rr] = mu;
+          t.micro[l].rstd[rr] = rs;
+        }
+      }
+      epi_bar();
+    };
+    // exact LN output of the thread's own d-space item (dW1 operand stash, read by W_j only)
+    auto ln_stash = [&](const float* y, int l) {
+      const SLayer& Ly = t.layers[l];
+      const float g = Ly.gamma[fo], b = Ly.beta[fo];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = 4 * ew + e;
+        if (r < M) t.micro[l].hop[(size_t)r * d + fo] = __float2bfloat16_rn(g * ((y[e] - rmu[r]) * rrs[r]) + b);
+      }
     };
 
     const bool own_d = slab * 128 < d, own_h = slab * 128 < H;
     if (!t.bwd) {
       // ---------------------------------------------------------------- forward task
+      float yk[4] = {0.f, 0.f, 0.f, 0.f};  // the thread's d-space item of the current block input
       if (own_d) {
-        float x[4];
+        const float zero[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int r = 4 * ew + e;
-          x[e] = r < M ? __ldcg(t.micro[0].x + (size_t)r * d + fo) : 0.0f;
+          yk[e] = r < M ? __ldcg(t.micro[0].x + (size_t)r * d + fo) : 0.0f;
         }
-        layernorm(x, 0, 0, 1);
+        ln_produce(yk, zero, 0);
       }
       for (int l = 0; l < t.L; ++l) {
         const SLayer& Ly = t.layers[l];
         const SMicro& Mi = t.micro[l];
         cur_p = 2 * l;
-        if (own_h) {  // GEMM1 epilogue: a = acc + b1; g = dropout(GELU(a))
-          const float b1 = Ly.b1[fo];
+        if (own_h) {  // GEMM1 epilogue: a = rs (acc - (mu - mu~) c) + e; g = dropout(GELU(a))
+          const float cf = Ly.cfold[fo], ef = Ly.efold[fo];
           const uint32_t step = Ly.drop_thresh ? *t.step : 0u;
+          ln_rows(l);  // while GEMM1 streams: its row statistics are only needed by this epilogue
           float acc[4];
           gemm_result(acc);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int r = 4 * ew + e;
             if (r >= M) continue;
-            const float z = acc[e] + b1;
+            const float z = rrs[r] * (acc[e] - (rmu[r] - rmp[r]) * cf) + ef;
             acc[e] = z;
             float gv = gelu_f(z);
             if (Ly.drop_thresh) {
@@ -440,32 +470,34 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             Mi.gop[(size_t)r * H + fo] = __float2bfloat16_rn(gv);
           }
           signal(2 + 3 * l, fo / (H / 4));
-          // the pre-activation is only read by the backward task: stored off the critical path
+          // read only by the backward task / W_j: stored off the critical path
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if (4 * ew + e < M) Mi.a[(size_t)(4 * ew + e) * H + fo] = acc[e];
+        } else if (own_d) {
+          ln_rows(l);
         }
+        if (own_d) ln_stash(yk, l);
         cur_p = 2 * l + 1;
-        if (own_d) {  // GEMM2 epilogue: y = x + acc + b2, then LN of the next block
+        if (own_d) {  // GEMM2 epilogue: y = x + acc + b2, then the next block's LN operand
           const float b2 = Ly.b2[fo];
-          float xr[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int r = 4 * ew + e;
-            xr[e] = r < M ? __ldcg(Mi.x + (size_t)r * d + fo) : 0.0f;
-          }
-          float acc[4], y[4];
+          float acc[4];
           gemm_result(acc);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int r = 4 * ew + e;
-            y[e] = r < M ? acc[e] + b2 + xr[e] : 0.0f;
+            yk[e] = r < M ? acc[e] + b2 + yk[e] : 0.0f;
           }
-          if (l + 1 < t.L) layernorm(y, l + 1, 3 + 3 * l, 4 + 3 * l);
+          if (l + 1 < t.L) {
+            float mut[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) mut[e] = rmu[4 * ew + e];
+            ln_produce(yk, mut, l + 1);
+          }
           // the residual stream is read by this thread (next block) and later tasks only
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (4 * ew + e < M) Mi.y[(size_t)(4 * ew + e) * d + fo] = y[e];
+            if (4 * ew + e < M) Mi.y[(size_t)(4 * ew + e) * d + fo] = yk[e];
         }
       }
     } else {
@@ -596,6 +628,45 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
   __syncthreads();
   cluster_sync();
   if (warp == 1) tmem_dealloc(tmem, 32);
+}
+
+// c[h] = sum_k gamma[k] W1[h][k], e[h] = sum_k beta[k] W1[h][k] + b1[h]: one warp per row, lanes
+// stride the row in 8-element vectors, fixed-order sums (deterministic)
+__global__ void __launch_bounds__(256) task_stream_fold_kernel(const __nv_bfloat16* __restrict__ W, int d, int H,
+                                                               const float* __restrict__ gamma,
+                                                               const float* __restrict__ beta,
+                                                               const float* __restrict__ b1, float* c, float* e) {
+  const int h = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (h >= H) return;
+  float sc = 0.0f, se = 0.0f;
+  for (int k = lane * 8; k < d; k += 256) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(W + (size_t)h * d + k);
+    const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+    const float4 g0 = *reinterpret_cast<const float4*>(gamma + k), g1 = *reinterpret_cast<const float4*>(gamma + k + 4);
+    const float4 b0 = *reinterpret_cast<const float4*>(beta + k), b1v = *reinterpret_cast<const float4*>(beta + k + 4);
+    const float2 w0 = __bfloat1622float2(w2[0]), w1 = __bfloat1622float2(w2[1]);
+    const float2 w2f = __bfloat1622float2(w2[2]), w3 = __bfloat1622float2(w2[3]);
+    sc += g0.x * w0.x + g0.y * w0.y + g0.z * w1.x + g0.w * w1.y + g1.x * w2f.x + g1.y * w2f.y + g1.z * w3.x + g1.w * w3.y;
+    se += b0.x * w0.x + b0.y * w0.y + b0.z * w1.x + b0.w * w1.y + b1v.x * w2f.x + b1v.y * w2f.y + b1v.z * w3.x +
+          b1v.w * w3.y;
+  }
+  sc = wsum32(sc);
+  se = wsum32(se);
+  if (lane == 0) {
+    c[h] = sc;
+    e[h] = se + b1[h];
+  }
+}
+
+int task_stream_fold(cudaStream_t st, const __nv_bfloat16* W1, int d, int H, const float* gamma, const float* beta,
+                     const float* b1, float* c, float* e) {
+  task_stream_fold_kernel<<<(H + 7) / 8, 256, 0, st>>>(W1, d, H, gamma, beta, b1, c, e);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    set_error("task_stream_fold launch: %s", cudaGetErrorString(err));
+    return -3;
+  }
+  return 0;
 }
 
 // ---------------------------------------------------------------------------------------- host

@@ -18,12 +18,16 @@ struct alignas(64) SLayer {
   CUtensorMap gop;   // Gop  [max_batch][H] bf16, box {64, 16}  (activation = GEMM2 operand, dW2 stash)
   CUtensorMap dyop;  // dYop [max_batch][d] bf16, box {64, 16}  (output grad = dG operand, dW2 stash)
   CUtensorMap daop;  // dAop [max_batch][H] bf16, box {64, 16}  (pre-act grad = dH operand, dW1 stash)
+  CUtensorMap ygm;   // yg [16][d] bf16, box {64, 16}: forward GEMM1 operand gamma (y - mu~) (task scratch)
   CUtensorMap w1c;   // diagnostics: W1 viewed as contiguous 16 KB tiles [H*d/64][64], box {64, 128}
   CUtensorMap w2c;   // diagnostics: W2 likewise
   const float* gamma;
   const float* beta;
   const float* b1;
   const float* b2;
+  const float* cfold;  // [H] c_h = sum_k gamma_k W1[h][k]  (fp32 over the bf16 weights)
+  const float* efold;  // [H] e_h = sum_k beta_k W1[h][k] + b1[h]
+  __nv_bfloat16* yg;   // [16][d] GEMM1 operand scratch (the memory behind ygm)
   uint32_t drop_thresh;  // dropout after GELU: keep iff (philox word >> 8) >= thresh (0 = none)
   float drop_scale;
   uint32_t site;         // global layer index (Philox counter word 2)
@@ -68,5 +72,9 @@ int task_stream_counter_bytes(int L);
 // Clusters of 4 the device can co-schedule (0 if the kernel cannot run there).
 int task_stream_max_clusters(int dev);
 int task_stream_launch(cudaStream_t st, const STask& t, int clusters);
+// c[h] = sum_k gamma[k] W1[h][k], e[h] = sum_k beta[k] W1[h][k] + b1[h] (fixed-order fp32 sums over
+// the bf16 weights; one warp per row)
+int task_stream_fold(cudaStream_t st, const __nv_bfloat16* W1, int d, int H, const float* gamma, const float* beta,
+                     const float* b1, float* c, float* e);
 
 }  // namespace tgp
