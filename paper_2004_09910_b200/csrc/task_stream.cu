@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
     int n = 0, cur_p = 0;
     auto epi_bar = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
     auto signal = [&](int id, int q) {
+      if (et == 0) dbg_stamp(t, cur_p, 9);
       epi_bar();
       if (et == 0) {
         // release: the epilogue barrier orders the other threads' stores before this reduction
@@ -357,16 +358,14 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
     // producer side (owners of the block input, d-space): chunk statistics (mean, M2 over the 32
     // features) and the operand gamma (y - mu~), then the quarter counter (operand) and the global
     // counter (statistics).  mut[e] = mu~ of row 4ew+e.
-    auto ln_produce = [&](const float* y, const float* mut, int l) {
-      const SLayer& Ly = t.layers[l];
+    auto ln_produce = [&](const float* y, const float* mut, int l, float g, __nv_bfloat16* yg) {
       const int J = d / 32;
       float* st = t.stats + (size_t)l * J * 32;
-      const float g = Ly.gamma[fo];
       // the operand first (critical path: the next GEMM1's activation tiles), statistics after
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = 4 * ew + e;
-        Ly.yg[(size_t)r * d + fo] = __float2bfloat16_rn(r < M ? g * (y[e] - mut[e]) : 0.0f);
+        yg[(size_t)r * d + fo] = __float2bfloat16_rn(r < M ? g * (y[e] - mut[e]) : 0.0f);
       }
       signal(1 + 3 * l, fo / (d / 4));
 #pragma unroll
@@ -444,15 +443,21 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           const int r = 4 * ew + e;
           yk[e] = r < M ? __ldcg(t.micro[0].x + (size_t)r * d + fo) : 0.0f;
         }
-        ln_produce(yk, zero, 0);
+        ln_produce(yk, zero, 0, t.layers[0].gamma[fo], t.layers[0].yg);
       }
       for (int l = 0; l < t.L; ++l) {
         const SLayer& Ly = t.layers[l];
         const SMicro& Mi = t.micro[l];
         cur_p = 2 * l;
         if (own_h) {  // GEMM1 epilogue: a = rs (acc - (mu - mu~) c) + e; g = dropout(GELU(a))
+          // every descriptor field the epilogue needs is loaded before the wait (no pointer chase
+          // through global memory after the GEMM result)
           const float cf = Ly.cfold[fo], ef = Ly.efold[fo];
-          const uint32_t step = Ly.drop_thresh ? *t.step : 0u;
+          const uint32_t dth = Ly.drop_thresh, site = Ly.site;
+          const float dsc = Ly.drop_scale;
+          const uint32_t step = dth ? *t.step : 0u;
+          __nv_bfloat16* const gop = Mi.gop;
+          float* const aout = Mi.a;
           ln_rows(l);  // while GEMM1 streams: its row statistics are only needed by this epilogue
           float acc[4];
           gemm_result(acc);
@@ -463,17 +468,17 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             const float z = rrs[r] * (acc[e] - (rmu[r] - rmp[r]) * cf) + ef;
             acc[e] = z;
             float gv = gelu_f(z);
-            if (Ly.drop_thresh) {
+            if (dth) {
               const uint64_t idx = (uint64_t)(t.r0 + r) * (uint64_t)H + (uint64_t)fo;
-              gv = dropout_keep(t.seed, step, Ly.site, idx, Ly.drop_thresh) ? gv * Ly.drop_scale : 0.0f;
+              gv = dropout_keep(t.seed, step, site, idx, dth) ? gv * dsc : 0.0f;
             }
-            Mi.gop[(size_t)r * H + fo] = __float2bfloat16_rn(gv);
+            gop[(size_t)r * H + fo] = __float2bfloat16_rn(gv);
           }
           signal(2 + 3 * l, fo / (H / 4));
           // read only by the backward task / W_j: stored off the critical path
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (4 * ew + e < M) Mi.a[(size_t)(4 * ew + e) * H + fo] = acc[e];
+            if (4 * ew + e < M) aout[(size_t)(4 * ew + e) * H + fo] = acc[e];
         } else if (own_d) {
           ln_rows(l);
         }
@@ -481,6 +486,10 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
         cur_p = 2 * l + 1;
         if (own_d) {  // GEMM2 epilogue: y = x + acc + b2, then the next block's LN operand
           const float b2 = Ly.b2[fo];
+          const bool more = l + 1 < t.L;
+          const float gnext = more ? t.layers[l + 1].gamma[fo] : 0.0f;
+          __nv_bfloat16* const yg = Ly.yg;
+          float* const yout = Mi.y;
           float acc[4];
           gemm_result(acc);
 #pragma unroll
@@ -488,16 +497,16 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             const int r = 4 * ew + e;
             yk[e] = r < M ? acc[e] + b2 + yk[e] : 0.0f;
           }
-          if (l + 1 < t.L) {
+          if (more) {
             float mut[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) mut[e] = rmu[4 * ew + e];
-            ln_produce(yk, mut, l + 1);
+            ln_produce(yk, mut, l + 1, gnext, yg);
           }
           // the residual stream is read by this thread (next block) and later tasks only
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (4 * ew + e < M) Mi.y[(size_t)(4 * ew + e) * d + fo] = yk[e];
+            if (4 * ew + e < M) yout[(size_t)(4 * ew + e) * d + fo] = yk[e];
         }
       }
     } else {
@@ -521,7 +530,11 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
         const SMicro& Mi = t.micro[l];
         cur_p = 2 * k;
         if (own_h) {  // dG epilogue: dA = dG * dropout mask * GELU'(a)
-          const uint32_t step = Ly.drop_thresh ? *t.step : 0u;
+          const uint32_t dth = Ly.drop_thresh, site = Ly.site;
+          const float dsc = Ly.drop_scale;
+          const uint32_t step = dth ? *t.step : 0u;
+          __nv_bfloat16* const daop = Mi.daop;
+          float* const pb = Mi.pb;
           float av[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -536,15 +549,15 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             da[e] = 0.0f;
             if (r >= M) continue;
             float dg = acc[e];
-            if (Ly.drop_thresh) {
+            if (dth) {
               const uint64_t idx = (uint64_t)(t.r0 + r) * (uint64_t)H + (uint64_t)fo;
-              dg = dropout_keep(t.seed, step, Ly.site, idx, Ly.drop_thresh) ? dg * Ly.drop_scale : 0.0f;
+              dg = dropout_keep(t.seed, step, site, idx, dth) ? dg * dsc : 0.0f;
             }
             da[e] = dg * gelu_df(av[e]);
-            Mi.daop[(size_t)r * H + fo] = __float2bfloat16_rn(da[e]);
+            daop[(size_t)r * H + fo] = __float2bfloat16_rn(da[e]);
           }
           signal(2 + 3 * k, fo / (H / 4));
-          colsums(da, nullptr, nullptr, Mi.pb, nullptr, nullptr);
+          colsums(da, nullptr, nullptr, pb, nullptr, nullptr);
         }
         cur_p = 2 * k + 1;
         if (own_d) {  // dH epilogue: LayerNorm backward + residual
@@ -564,6 +577,10 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
               nv[e] = gyv[e] = rsv[e] = 0.0f;
             }
           }
+          float* const pg = Mi.pg;
+          float* const pbt = Mi.pbt;
+          __nv_bfloat16* const dyn = l > 0 ? t.micro[l - 1].dyop : nullptr;
+          float* const pb2n = l > 0 ? t.micro[l - 1].pb2 : nullptr;
           float dh[4], dhn[4], dn[4];
           gemm_result(dh);
           const int J = d / 32;
@@ -578,7 +595,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             if (lane == 0) *reinterpret_cast<float2*>(st + ((size_t)chunk * 16 + 4 * ew + e) * 2) = make_float2(s1, s2);
           }
           signal(3 + 3 * k, 4);
-          colsums(dhn, dh, nullptr, Mi.pg, Mi.pbt, nullptr);
+          colsums(dhn, dh, nullptr, pg, pbt, nullptr);
           wait_cnt(3 + 3 * k, 4, (unsigned)J);
           {
             const int rr = et >> 3, jl = et & 7;
@@ -609,14 +626,13 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             dxv[e] = gyv[e] + rsv[e] * (dn[e] - rmu[r] - nv[e] * rrs[r]);
           }
           if (l > 0) {  // the next block's dG operand first (critical path), then the rest
-            const SMicro& Mn = t.micro[l - 1];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int r = 4 * ew + e;
-              if (r < M) Mn.dyop[(size_t)r * d + fo] = __float2bfloat16_rn(dxv[e]);
+              if (r < M) dyn[(size_t)r * d + fo] = __float2bfloat16_rn(dxv[e]);
             }
             signal(4 + 3 * k, fo / (d / 4));
-            colsums(dxv, nullptr, nullptr, Mn.pb2, nullptr, nullptr);
+            colsums(dxv, nullptr, nullptr, pb2n, nullptr, nullptr);
           }
 #pragma unroll
           for (int e = 0; e < 4; ++e)

@@ -41,7 +41,7 @@ L.tgp_debug_stream_read(P.h, 0, buf.ctypes.data, n.value, ctypes.byref(n))
 NP = 2 * blocks
 G = n.value // (NP * 10)
 ev = buf.reshape(G, NP, 10).astype(np.int64)
-names = ["B issue", "W first", "W last", "B landed", "MMA done", "TMEM rdy", "partials", "signal", "stats"]
+names = ["B issue", "W first", "W last", "B landed", "MMA done", "TMEM rdy", "partials", "signal", "stats", "sig entry"]
 t0 = ev[:, 0, 1].min()
 print(f"{'bwd' if bwd else 'fwd'} task, {blocks} blocks, {G} CTAs, variant={opts.get('variant', 0)}")
 prev = None
