@@ -52,10 +52,27 @@ struct TcCfg {
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
+TGP_DEV void tma_store_2d(const void* desc, const void* smem, int32_t c0, int32_t c1, bool reduce_add) {
+  if (reduce_add)
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(desc),
+                 "r"(c0), "r"(c1), "r"(smem_u32(smem))
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(desc), "r"(c0),
+                 "r"(c1), "r"(smem_u32(smem))
+                 : "memory");
+}
+TGP_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+TGP_DEV void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
 template <int BN, bool A_MN, bool B_MN, int MODE>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
-                   const __grid_constant__ CUtensorMap tmB1, const GemmParams p) {
+                   const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmD,
+                   const GemmParams p) {
   using C = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -242,33 +259,38 @@ __global__ void __launch_bounds__(192, 1)
     const int fl = lg * 32 + lane;
     const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
     if constexpr (MODE == EPI_DW) {
-      const EpiParams& e = p.epi;
-      const int m = m0 + fl;
-      float* row = e.dw + (int64_t)m * e.ldw + nb;
+      // fp32 tile -> shared memory (128-byte swizzled [128 rows][32 cols] chunks, double-buffered
+      // in the now idle pipeline stages) -> TMA tensor store, or TMA reduce-add into the existing
+      // gradient when accumulating (the read-modify-write happens in L2); full 128-byte row
+      // segments instead of 32 row-strided 16-byte stores per warp instruction
+      const bool leader = threadIdx.x == 64;
+      const bool acc = p.epi.accumulate != 0;
 #pragma unroll 1
-      for (int c = 0; c < BN / 16; ++c) {
-        float v[16];
-        tmem_ld16(taddr + c * 16, v);
+      for (int c = 0; c < BN / 32; ++c) {
+        uint8_t* buf = smem + (c & 1) * 16384;
+        if (c >= 2) {
+          if (leader) bulk_wait_read<1>();  // the store issued from this buffer has read it
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+        float v[32];
+        tmem_ld16(taddr + c * 32, v);
+        tmem_ld16(taddr + c * 32 + 16, v + 16);
         if (nkb == 0) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+          for (int i = 0; i < 32; ++i) v[i] = 0.0f;
         }
-        if (nb + c * 16 < p.N && m < p.M) {
-          float4* dst = reinterpret_cast<float4*>(row + c * 16);
+        uint8_t* row = buf + fl * 128;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            if (e.accumulate) {
-              float4 old = dst[q];
-              o.x += old.x;
-              o.y += old.y;
-              o.z += old.z;
-              o.w += old.w;
-            }
-            dst[q] = o;
-          }
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(row + ((q ^ (fl & 7)) << 4)) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        fence_proxy_async();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (leader && nb + c * 32 < p.N) {
+          tma_store_2d(&tmD, buf, nb + c * 32, m0, acc);
+          bulk_commit();
         }
       }
+      if (leader) bulk_wait_read<0>();
     } else if constexpr (C::PUSH) {
       // push: every rank STORES the slice of its partial tile owned by rank `owner` (features
       // [owner*rpr, +rpr)) into the owner's dedicated receive region, slot = source rank:
@@ -448,7 +470,7 @@ bool make_map(CUtensorMap* map, const TcMat& t, int box_inner, int box_outer, bo
 
 template <int BN, bool A_MN, bool B_MN, int MODE>
 static int launch_tc(cudaStream_t st, bool pdl, const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
-                     const GemmParams& p, int S, int ntiles) {
+                     const CUtensorMap& dmap, const GemmParams& p, int S, int ntiles) {
   using C = TcCfg<BN>;
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, MODE>;
   static bool attr_done = false;
@@ -474,7 +496,7 @@ static int launch_tc(cudaStream_t st, bool pdl, const CUtensorMap& a, const CUte
   attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = pdl ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b0, b1, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b0, b1, dmap, p);
   if (e != cudaSuccess) {
     set_error("gemm_tc launch (BN=%d A_MN=%d B_MN=%d grid=%d,%d,%d): %s", BN, (int)A_MN, (int)B_MN, p.M / 128, S,
               ntiles, cudaGetErrorString(e));
@@ -537,12 +559,28 @@ int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B
   } else {
     mb1 = mb0;
   }
+  CUtensorMap md = mb0;  // dW: fp32 [M][ldw] output, box {32 cols, 128 rows}, 128-byte swizzle
+  if (dw) {
+    const Driver* drv = driver();
+    if (!drv) return -3;
+    cuuint64_t dims[2] = {(cuuint64_t)p.N, (cuuint64_t)p.M};
+    cuuint64_t strides[1] = {(cuuint64_t)p.epi.ldw * 4};
+    cuuint32_t box[2] = {32, 128};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = drv->tensorMapEncodeTiled(&md, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, p.epi.dw, dims, strides, box, es,
+                                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("dW output tensor map failed (%d): M=%d N=%d ldw=%lld", (int)r, p.M, p.N, (long long)p.epi.ldw);
+      return -3;
+    }
+  }
   // instantiated for the (operand majors, epilogue mode) pairs the runtime uses: forward
   // W[out][in] x X[rows][in] (K-major, K-major), backward W^T x dY (MN-major, K-major), deferred dW
   // dY^T x X (MN-major, MN-major)
   const int mode = p.epi.mode;
 #define TGP_LAUNCH_M(BNv, AM, BM, MD) \
-  if (BN == BNv && a_mn == AM && b_mn == BM && mode == MD) return launch_tc<BNv, AM, BM, MD>(st, pdl, ma, mb0, mb1, p, S, ntiles);
+  if (BN == BNv && a_mn == AM && b_mn == BM && mode == MD) return launch_tc<BNv, AM, BM, MD>(st, pdl, ma, mb0, mb1, md, p, S, ntiles);
 #define TGP_LAUNCH(BNv)                                  \
   TGP_LAUNCH_M(BNv, false, false, EPI_LINEAR_FWD)        \
   TGP_LAUNCH_M(BNv, false, false, EPI_RESID_FWD)         \

@@ -252,6 +252,10 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           tc_fence_after();
           if (kb == 0) dbg_stamp(t, p, 3);
           const uint32_t a = smem_u32(ring + s * ST_STAGE), b = a + ST_A;
+          if (t.flags & 1024) {  // timing experiment: no MMA, release the stage at once
+            mbar_arrive(&empty[s]);
+            continue;
+          }
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint64_t ad = t.bwd ? make_sdesc_sw128(a + kk * 2048, 8192, 1024) : make_sdesc_sw128(a + kk * 32, 16, 1024);

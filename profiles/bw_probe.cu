@@ -106,18 +106,34 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   struct Cfg {
-    int grid, chunk, nst, mode;
-  } cfgs[] = {{128, 16384, 10, 0}, {148, 16384, 10, 0}, {128, 16384, 10, 1}, {148, 16384, 10, 1},
+    int grid, chunk, nst, mode, cluster;
+  } cfgs[] = {{128, 16384, 10, 2, 4}, {128, 16384, 11, 2, 4}, {128, 16384, 10, 0, 4}, {128, 16384, 10, 1, 4},
+              {148, 16384, 10, 1, 4}, {128, 32768, 6, 1, 4}, {128, 32768, 6, 1, 2},{128, 16384, 10, 0}, {148, 16384, 10, 0}, {128, 16384, 10, 1}, {148, 16384, 10, 1},
               {296, 16384, 5, 1},  {128, 32768, 6, 1},  {148, 32768, 6, 1},  {128, 8192, 20, 1},
               {128, 16384, 4, 1},  {128, 16384, 13, 1}, {148, 16384, 13, 1}, {128, 16384, 10, 2},
-              {128, 16384, 13, 2}, {256, 16384, 6, 2}};
+              {128, 16384, 13, 2}, {256, 16384, 6, 2}, {128, 16384, 10, 2, 2}};
   for (const Cfg& k : cfgs) {
     const size_t smem = (size_t)k.chunk * k.nst + 1024 + 512;
     float best = 1e9;
     const size_t bytes = (k.mode == 2) ? (total / 4) : total;  // mode 2 reads a 256 MiB matrix view
     for (int rep = 0; rep < 5; ++rep) {
       cudaEventRecord(a);
-      probe<<<k.grid, 64, smem>>>(buf, bytes, k.chunk, k.nst, k.mode, tm);
+      if (k.cluster > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(k.grid);
+        cfg.blockDim = dim3(64);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = k.cluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, probe, (const char*)buf, bytes, k.chunk, k.nst, k.mode, tm);
+      } else {
+        probe<<<k.grid, 64, smem>>>(buf, bytes, k.chunk, k.nst, k.mode, tm);
+      }
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
@@ -125,7 +141,7 @@ int main() {
       if (ms < best) best = ms;
     }
     cudaError_t e = cudaGetLastError();
-    printf("grid %3d chunk %5d stages %2d mode %d: %.1f GB/s %s\n", k.grid, k.chunk, k.nst, k.mode,
+    printf("grid %3d cluster %d chunk %5d stages %2d mode %d: %.1f GB/s %s\n", k.grid, k.cluster, k.chunk, k.nst, k.mode,
            bytes / (best * 1e-3) / 1e9, e == cudaSuccess ? "" : cudaGetErrorString(e));
   }
   return 0;

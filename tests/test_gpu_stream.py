@@ -88,3 +88,35 @@ def test_stream_full_c2_width_parity():
     ref = oracle_step(layers, params, x, t, lr=0.05, m=32, seed=1234, step=0)
     errs, bad = compare(g, ref, params, TOL, 0.05)
     assert not bad, bad
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_gradients_accumulate_across_backward_calls(dtype):
+    # "gradients accumulate across forward/backward pairs until step": the deferred dW
+    # of the second backward adds into the first (TMA reduce-add epilogue), bias / LN partials too
+    import torch
+
+    from paper_2004_09910_b200 import Pipeline
+
+    layers = C.resmlp_stack(2, 512, hidden=1024)
+    B, m = 64, 4
+    x, t, params = make_case(layers, B, 21, dtype)
+    ref = oracle_step(layers, params, x, t, lr=0.05, m=m, seed=21, step=0)
+    P = Pipeline(layers, chunks=m, devices=[0], checkpoint="except_last", max_batch=B, dtype=dtype, seed=21)
+    for i, p in enumerate(params):
+        P.set_param(i, p)
+    X = torch.tensor(np.asarray(x, np.float32), device="cuda")
+    T = torch.tensor(np.asarray(t, np.float32), device="cuda")
+    Y = torch.empty(B, 512, device="cuda")
+    DY = torch.empty_like(Y)
+    for _ in range(2):
+        P.forward(X, B, Y)
+        P.mse_loss_grad(Y, T, B, DY)
+        P.backward(DY)
+    tol = 2e-2 if dtype == "bf16" else 1e-4
+    scale = max(np.max(np.abs(g)) for g in ref["grads"])
+    for k, gr in enumerate(ref["grads"]):
+        g = P.get_grad(k)
+        e = np.max(np.abs(g - 2.0 * np.asarray(gr).ravel())) / max(2.0 * np.max(np.abs(gr)), 1e-3 * scale)
+        assert e <= tol, (k, e)
+    P.close()
