@@ -1,0 +1,3 @@
+for v in 0 1 2048 2049; do timeout 120 python profiles/st_phases.py blocks=32 variant=$v | tail -1 | sed "s/^/fwd variant $v: /"; done
+timeout 120 python profiles/st_phases.py blocks=32 bwd=1 | tail -1 | sed "s/^/bwd: /"
+timeout 120 python profiles/st_phases.py blocks=4 variant=1 2>&1 | head -6

@@ -1,0 +1,19 @@
+"""F-task time of the stream kernel (no debug stamps) under test_stream_variant values.
+    python profiles/st_time.py v1 v2 ...   (bits: 1 nodep, 2 contiguous tiles, 1024 no MMA, 2048 no TMEM staging)"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402,F401
+
+from paper_2004_09910_b200 import Pipeline  # noqa: E402
+from synth import configs as C  # noqa: E402
+
+P = Pipeline(C.resmlp_stack(32, 4096), chunks=32, devices=[0], balance=[32], checkpoint="except_last", max_batch=512,
+             dtype="bf16", seed=1)
+P.init_params(1)
+for v in [int(a) for a in sys.argv[1:]] or [0]:
+    P.set_option("test_stream_variant", v)
+    P.bench_dominant_gemm(0, 512, reps=2)
+    ms, by, n = P.bench_dominant_gemm(0, 512, reps=10)
+    print(f"variant {v:5d}: F task {ms * 1e3:7.1f} us = {ms * 1e3 / 64:5.2f} us/phase, {by / ms / 1e6:6.0f} GB/s")
