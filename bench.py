@@ -243,6 +243,12 @@ def run_tgp(args):
     else:
         peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
     achieved = gemm_bytes / (gemm_ms * 1e-3) / 1e9
+    traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
+    if stream:
+        try:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "stream_traffic.json")))["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         v, cores, desc = cpu_oracle_sample(steps=1, blocks=args.ref_blocks)
@@ -258,7 +264,7 @@ def run_tgp(args):
                     "h2d_bytes_per_step": 4 * BATCH * WIDTH * 2, "d2h_bytes_per_step": 8},
             "gpu_launches": int(nk),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": kname,
+                         "traffic": traffic, "kernel": kname,
                          "algorithmic_bytes_per_launch": gemm_bytes, "avg_launch_us": gemm_ms * 1e3,
                          "launches_timed": gemm_n, "peak_source": peak_src},
             "clocks": clocks,
