@@ -321,13 +321,19 @@ static int st_build_desc(tgp_ctx* c, Stage& s, int B) {
         !make_map(&P.daop, TcMat{Ly.dAop, c->max_batch, H, H}, 64, 16))
       return TGP_E_CUDA;
     if (!make_map(&P.ygm, TcMat{s.st_yg, 16, d, d}, 64, 16)) return TGP_E_CUDA;
+    if (!make_map(&P.ucm, TcMat{s.st_uc, 32, d, d}, 64, 32)) return TGP_E_CUDA;
     P.gamma = mparam(s, Ly, 0);
     P.beta = mparam(s, Ly, 1);
     P.b1 = mparam(s, Ly, 3);
     P.b2 = mparam(s, Ly, 5);
-    P.cfold = s.st_fold + (size_t)(l - s.l0) * 2 * H;
+    P.cfold = s.st_fold + (size_t)(l - s.l0) * 3 * H;
     P.efold = P.cfold + H;
+    P.c2fold = P.cfold + 2 * H;
+    P.c2part = s.st_c2part + (size_t)(l - s.l0) * (d / 256) * H;
+    P.w2 = (const __nv_bfloat16*)w2;
+    P.uc = (__nv_bfloat16*)s.st_uc;
     P.yg = (__nv_bfloat16*)s.st_yg;
+    P.w1 = (const __nv_bfloat16*)w1;
     P.drop_thresh = drop_thresh(Ly.L.dropout);
     P.drop_scale = Ly.L.dropout > 0 ? 1.0f / (1.0f - Ly.L.dropout) : 1.0f;
     P.site = (uint32_t)l;
@@ -368,16 +374,12 @@ static bool use_stream(const tgp_ctx* c, const Stage& s, int M) { return s.st_ok
 
 // LayerNorm folded into GEMM1 of the stream kernel: recompute c = W1 gamma, e = W1 beta + b1 of
 // every block after the weights or LN parameters changed (SGD step, set / init).
-static int st_refold(tgp_ctx* c, Stage& s) {
+static int st_refold(tgp_ctx* c, Stage& s, int B) {
   if (!s.st_ok || !s.fold_dirty) return 0;
-  for (int l = s.l0; l < s.l1; ++l) {
-    LayerRT& Ly = c->layers[l];
-    const int d = Ly.L.d_in, H = Ly.L.d_hidden;
-    float* cf = s.st_fold + (size_t)(l - s.l0) * 2 * H;
-    TGP_TRY(task_stream_fold(s.comp, (const __nv_bfloat16*)wparam(c, s, Ly, 2), d, H, mparam(s, Ly, 0),
-                             mparam(s, Ly, 1), mparam(s, Ly, 3), cf, cf + H));
-    c->kernels++;
-  }
+  if (s.st_micro_B != B) TGP_TRY(st_build_desc(c, s, B));
+  const LayerRT& L0 = c->layers[s.l0];
+  TGP_TRY(task_stream_fold(s.comp, (const SLayer*)s.st_layers, s.l1 - s.l0, L0.L.d_in, L0.L.d_hidden));
+  c->kernels++;
   s.fold_dirty = false;
   return 0;
 }

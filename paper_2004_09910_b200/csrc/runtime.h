@@ -109,8 +109,10 @@ struct Stage {
   int st_micro_B = -1;
   float* st_stats = nullptr;
   unsigned* st_cnt = nullptr;
-  float* st_fold = nullptr;   // per block [2][H]: LN folded into GEMM1 (c = W1 gamma, e = W1 beta + b1)
+  float* st_fold = nullptr;   // per block [3][H]: c = W1 gamma, e = W1 beta + b1 (R3), c2 = 1^T W2 (R4)
   void* st_yg = nullptr;      // [16][d] bf16: GEMM1 operand gamma (y - mu~) of the current block
+  void* st_uc = nullptr;      // [32][d] bf16: backward dG operand [u | n]
+  float* st_c2part = nullptr; // [L][d/256][H] partial column sums of W2
   bool fold_dirty = true;     // weights / LN parameters changed since st_fold was computed
   unsigned long long* st_dbg = nullptr;  // diagnostics (TGP_ST_DEBUG): [grid][2L][ST_DBG_SLOTS]
   std::vector<TaskGraph> gF, gB;

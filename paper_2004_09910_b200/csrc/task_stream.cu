@@ -38,6 +38,8 @@
 //                 dgamma, dbeta column sums; [l > 0] dY_{l-1} = dx bf16, db2 sums (id 4 + 3k)
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "host.h"
 #include "kernels.h"
@@ -48,13 +50,13 @@ namespace tgp {
 namespace {
 constexpr int SK = 4;                       // split-K ranks per cluster
 constexpr int ST_A = 16384;                 // 128 x 64 bf16 weight tile
-constexpr int ST_B = 2048;                  // 16 x 64 bf16 activation tile of the same k-block
-constexpr int ST_STAGE = ST_A + ST_B;       // one ring stage (both 1024-byte aligned)
-constexpr int ST_STAGES = 11;               // ring depth
-constexpr int ST_RECV = SK * 32 * 16 * 4;   // owner receive buffer: [src][32 features][16 rows] fp32
-constexpr int OFF_RECV = ST_STAGES * ST_STAGE;
-constexpr int OFF_BAR = OFF_RECV + 2 * ST_RECV;
-constexpr int ST_SMEM = OFF_BAR + 3072 + 1024;
+// Shared-memory layout (runtime: the backward's dG phases have 32-row operands, see below)
+//   forward : 11 stages x (16 KB weight + 2 KB activation tile), 2 x  8 KB receive buffers
+//   backward:  9 stages x (16 KB weight + 4 KB activation tile), 2 x 16 KB receive buffers
+constexpr int ST_STAGES_MAX = 11;
+constexpr int ST_LAYOUT_FWD = 11 * (ST_A + 2048) + 2 * (SK * 32 * 16 * 4);
+constexpr int ST_LAYOUT_BWD = 9 * (ST_A + 4096) + 2 * (SK * 32 * 32 * 4);
+constexpr int ST_SMEM = (ST_LAYOUT_FWD > ST_LAYOUT_BWD ? ST_LAYOUT_FWD : ST_LAYOUT_BWD) + 3072 + 1024;
 constexpr int CNT_STRIDE = 32;              // uints between counters (one 128-byte line each)
 }  // namespace
 
@@ -94,23 +96,28 @@ TGP_DEV Ph phase_of(const STask& t, int p) {
   const int l = t.bwd ? t.L - 1 - k : k;
   const SLayer& Ly = t.layers[l];
   if (!t.bwd) return sub ? Ph{&Ly.w2k, &Ly.gop, t.H, t.d} : Ph{&Ly.w1k, &Ly.ygm, t.d, t.H};
-  return sub ? Ph{&Ly.w1m, &Ly.daop, t.H, t.d} : Ph{&Ly.w2m, &Ly.dyop, t.d, t.H};
+  return sub ? Ph{&Ly.w1m, &Ly.daop, t.H, t.d} : Ph{&Ly.w2m, &Ly.ucm, t.d, t.H};
 }
 
 __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_constant__ STask t) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int NST = t.bwd ? 9 : 11;                   // ring depth (divisions below use literals)
+  const int STG = ST_A + (t.bwd ? 4096 : 2048);     // ring stage bytes (weight tile + activation tile)
+  const int RECV = SK * 32 * (t.bwd ? 32 : 16) * 4;  // one receive buffer
+  const int OFF_RECV = NST * STG, OFF_BAR = OFF_RECV + 2 * RECV;
   uint8_t* ring = smem;
-  float* recv = reinterpret_cast<float*>(smem + OFF_RECV);  // [2][SK][32][16]
+  float* recv = reinterpret_cast<float*>(smem + OFF_RECV);  // [2][SK][32 features][ncols]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* empty = full + ST_STAGES;
-  uint64_t* tfull = empty + ST_STAGES;  // [2] TMEM accumulator ready
+  uint64_t* empty = full + ST_STAGES_MAX;
+  uint64_t* tfull = empty + ST_STAGES_MAX;  // [2] TMEM accumulator ready
   uint64_t* tempty = tfull + 2;         // [2] TMEM accumulator drained (128 arrivals)
   uint64_t* rbar = tempty + 2;          // [2] split-K partials of a phase received (owner)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
   float* rmu = reinterpret_cast<float*>(smem + OFF_BAR + 512);  // [16] row statistics
   float* rrs = rmu + 16;                                        // [16]
   float* cs = rrs + 16;                                         // [3][4][32] column-sum partials
+  float* rsb = cs + 3 * 4 * 32;  // [16] backward: rstd of the LN whose backward feeds the current dG
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)cluster_ctarank();
@@ -118,10 +125,21 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
   const int NP = 2 * t.L;
   const int d = t.d, H = t.H, M = t.M;
   auto active = [&](int p) { return slab * 128 < phase_of(t, p).F; };
+  // rows of a phase's activation operand / MMA N: the backward's dG phases take [u | n] (32 rows,
+  // LayerNorm backward folded, see the backward epilogue), every other phase the 16 micro-batch rows
+  auto ncol = [&](int p) { return (t.bwd && !(p & 1)) ? 32 : 16; };
+  // phase index of the k-th active phase of this CTA (NP if none), from a table built at start
+  uint16_t* act_list = reinterpret_cast<uint16_t*>(smem + OFF_BAR + 2560);  // [<= 256]
+  auto nth_active = [&](int k) { return k < NP ? (int)act_list[k] : NP; };
+  auto recv_bytes = [&](int p) { return (uint32_t)(SK * 32 * ncol(p) * 4); };
   auto cnt = [&](int id, int q) { return t.cnt + ((size_t)id * 5 + q) * CNT_STRIDE; };
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < ST_STAGES; ++s) {
+    int na = 0;
+    for (int p = 0; p < NP; ++p)
+      if (active(p)) act_list[na++] = (uint16_t)p;
+    for (int k = na; k < NP; ++k) act_list[k] = (uint16_t)NP;
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -132,10 +150,12 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
     }
     fence_barrier_init();
     // first use of each receive buffer: 4 sources x 32 features x 16 rows x 4 B
-    mbar_arrive_expect_tx(&rbar[0], ST_RECV);
-    mbar_arrive_expect_tx(&rbar[1], ST_RECV);
+    for (int b = 0; b < 2; ++b) {
+      const int p = nth_active(b);
+      if (p < NP) mbar_arrive_expect_tx(&rbar[b], recv_bytes(p));
+    }
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 32);
+  if (warp == 1) tmem_alloc(tmem_slot, 64);  // two accumulators of up to 32 columns
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // every rank's receive barriers are initialised before any st.async
@@ -155,10 +175,11 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
       auto load_b = [&](int p, int kb, int tile) {
         const Ph P = phase_of(t, p);
         const int nkb = P.K / (SK * 64);
-        const int s = tile % ST_STAGES;
-        // forward GEMM1 reads the [16][d] task scratch gamma (y - mu~) (row 0), all others the stash rows
-        const int row = (!t.bwd && !(p & 1)) ? 0 : t.r0;
-        tma_load_2d(P.B, &full[s], ring + s * ST_STAGE + ST_A, (rank * nkb + kb) * 64, row, pol_b);
+        const int s = t.bwd ? tile % 9 : tile % 11;
+        // forward GEMM1 reads the [16][d] task scratch gamma (y - mu~), the backward's dG the [32][d]
+        // scratch [u | n] (both row 0), all others the stash rows of the micro-batch
+        const int row = !(p & 1) ? 0 : t.r0;
+        tma_load_2d(P.B, &full[s], ring + s * STG + ST_A, (rank * nkb + kb) * 64, row, pol_b);
       };
       // optional L2 prefetch of the weight tiles `pfd` tiles ahead of the ring (test_stream_variant
       // bits 4-9; measured: any distance makes the task slower -- profiles/r1o_st_variants.txt)
@@ -180,7 +201,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           pq = next_active(pq + 1);
         }
       };
-      for (int q = 0; q < ST_STAGES + pfd && pfd > 0; ++q) prefetch_next();
+      for (int q = 0; q < NST + pfd && pfd > 0; ++q) prefetch_next();
       while (wp < NP || rp < NP) {
         bool progress = false;
         // poll the dependency of phase rp (issued first, used after the weight loop)
@@ -190,15 +211,15 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           have = (t.flags & 1) ? need : ld_relaxed_u32(cnt(1 + 3 * (rp >> 1) + (rp & 1), rank));
         }
         while (wp < NP) {  // weights: run ahead as far as the ring allows
-          const int s = it % ST_STAGES, r = it / ST_STAGES;
+          const int s = t.bwd ? it % 9 : it % 11, r = t.bwd ? it / 9 : it / 11;
           if (!mbar_test_wait(smem_u32(&empty[s]), (uint32_t)((r & 1) ^ 1))) break;
           const Ph P = phase_of(t, wp);
           const int nkb = P.K / (SK * 64);
           const int kc = (rank * nkb + wkb) * 64;
           if (wkb == 0) dbg_stamp(t, wp, 1);
           if (wkb == nkb - 1) dbg_stamp(t, wp, 2);
-          uint8_t* dst = ring + s * ST_STAGE;
-          mbar_arrive_expect_tx(&full[s], ST_STAGE);
+          uint8_t* dst = ring + s * STG;
+          mbar_arrive_expect_tx(&full[s], (uint32_t)(ST_A + 128 * ncol(wp)));
           if (t.flags & 2) {
             const SLayer& Ly = t.layers[t.bwd ? t.L - 1 - (wp >> 1) : (wp >> 1)];
             const CUtensorMap* cm = ((wp & 1) != t.bwd) ? &Ly.w2c : &Ly.w1c;
@@ -237,21 +258,23 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
   } else if (warp == 1) {
     if (elect_one()) {
       // ------------------------------------------------------------ MMA issuer (single thread)
-      const uint32_t idesc = t.bwd ? make_idesc_bf16(128, 16, true, false) : make_idesc_bf16(128, 16, false, false);
+      const uint32_t idesc16 = make_idesc_bf16(128, 16, t.bwd != 0, false);
+      const uint32_t idesc32 = make_idesc_bf16(128, 32, t.bwd != 0, false);
       int it = 0, n = 0;
       for (int p = 0; p < NP; ++p) {
         if (!active(p)) continue;
         const int nkb = phase_of(t, p).K / (SK * 64);
+        const uint32_t idesc = ncol(p) == 32 ? idesc32 : idesc16;
         const int buf = n & 1, u = n >> 1;
         mbar_wait(&tempty[buf], (uint32_t)((u & 1) ^ 1));
         tc_fence_after();
-        const uint32_t dacc = tmem + (uint32_t)(buf * 16);
+        const uint32_t dacc = tmem + (uint32_t)(buf * 32);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % ST_STAGES, r = it / ST_STAGES;
+          const int s = t.bwd ? it % 9 : it % 11, r = t.bwd ? it / 9 : it / 11;
           mbar_wait(&full[s], (uint32_t)(r & 1));
           tc_fence_after();
           if (kb == 0) dbg_stamp(t, p, 3);
-          const uint32_t a = smem_u32(ring + s * ST_STAGE), b = a + ST_A;
+          const uint32_t a = smem_u32(ring + s * STG), b = a + ST_A;
           if (t.flags & 1024) {  // timing experiment: no MMA, release the stage at once
             mbar_arrive(&empty[s]);
             continue;
@@ -314,42 +337,54 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
     };
     // result of the current GEMM phase for (fo, 4 rows): TMEM -> push slices to their owners ->
     // fixed-order sum of the 4 sources
-    auto gemm_result = [&](float* acc) {
+    // result of the current GEMM phase for (fo, rows 4ew..4ew+3) [and, 32-column phases, columns
+    // 16 + 4ew..]: TMEM -> push 32-feature slices to their owners -> fixed-order sum of the 4 sources
+    auto gemm_result = [&](auto NC, float* acc, float* acc2) {
       const int buf = n & 1, u = n >> 1;
+      constexpr int nc = decltype(NC)::value, nq = nc / 4;
       mbar_wait(&tfull[buf], (uint32_t)(u & 1));
       tc_fence_after();
       if (et == 0) dbg_stamp(t, cur_p, 5);
-      float v[16];
-      tmem_ld16(tmem + (uint32_t)(buf * 16) + ((uint32_t)(lg * 32) << 16), v);
+      float v[32];
+      tmem_ld16(tmem + (uint32_t)(buf * 32) + ((uint32_t)(lg * 32) << 16), v);
+      if constexpr (nc == 32) tmem_ld16(tmem + (uint32_t)(buf * 32 + 16) + ((uint32_t)(lg * 32) << 16), v + 16);
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
-      const uint32_t rb = smem_u32(recv + buf * (ST_RECV / 4));
+      const uint32_t rb = smem_u32(recv + buf * (RECV / 4));
       const uint32_t dbar = mapa_shared(smem_u32(&rbar[buf]), (uint32_t)lg);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t idx = (uint32_t)((rank * 32 + lane) * 4 + (q ^ (lane & 3)));
+      for (int q = 0; q < nq; ++q) {
+        const uint32_t idx = (uint32_t)((rank * 32 + lane) * nq + (q ^ (lane & (nq - 1))));
         st_async_f32x4(mapa_shared(rb + idx * 16u, (uint32_t)lg),
                        make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]), dbar);
       }
       mbar_wait(&rbar[buf], (uint32_t)(u & 1));
       if (et == 0) dbg_stamp(t, cur_p, 6);
-      const float4* r4 = reinterpret_cast<const float4*>(recv + buf * (ST_RECV / 4));
-      float4 a = r4[(0 * 32 + lane) * 4 + (ew ^ (lane & 3))];
+      const float4* r4 = reinterpret_cast<const float4*>(recv + buf * (RECV / 4));
 #pragma unroll
-      for (int s = 1; s < SK; ++s) {
-        const float4 b = r4[(s * 32 + lane) * 4 + (ew ^ (lane & 3))];
-        a.x += b.x;
-        a.y += b.y;
-        a.z += b.z;
-        a.w += b.w;
+      for (int h = 0; h < nc / 16; ++h) {
+        const int q = ew + 4 * h;
+        float4 a = r4[(0 * 32 + lane) * nq + (q ^ (lane & (nq - 1)))];
+#pragma unroll
+        for (int s = 1; s < SK; ++s) {
+          const float4 b = r4[(s * 32 + lane) * nq + (q ^ (lane & (nq - 1)))];
+          a.x += b.x;
+          a.y += b.y;
+          a.z += b.z;
+          a.w += b.w;
+        }
+        float* o = h ? acc2 : acc;
+        o[0] = a.x;
+        o[1] = a.y;
+        o[2] = a.z;
+        o[3] = a.w;
       }
       // re-arm for this buffer's next use (its pushes come only after every owner signalled
       // this phase, i.e. after the reads above)
-      if (et == 0) mbar_arrive_expect_tx(&rbar[buf], ST_RECV);
-      acc[0] = a.x;
-      acc[1] = a.y;
-      acc[2] = a.z;
-      acc[3] = a.w;
+      if (et == 0) {
+        const int pn = nth_active(n + 2);
+        if (pn < NP) mbar_arrive_expect_tx(&rbar[buf], recv_bytes(pn));
+      }
       ++n;
     };
     // Forward LayerNorm folded into GEMM1 (reading R3 in DESIGN.md).  With mu, rs the statistics
@@ -464,7 +499,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           float* const aout = Mi.a;
           ln_rows(l);  // while GEMM1 streams: its row statistics are only needed by this epilogue
           float acc[4];
-          gemm_result(acc);
+          gemm_result(std::integral_constant<int, 16>{}, acc, nullptr);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int r = 4 * ew + e;
@@ -495,7 +530,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           __nv_bfloat16* const yg = Ly.yg;
           float* const yout = Mi.y;
           float acc[4];
-          gemm_result(acc);
+          gemm_result(std::integral_constant<int, 16>{}, acc, nullptr);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int r = 4 * ew + e;
@@ -515,28 +550,70 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
       }
     } else {
       // ---------------------------------------------------------------- backward task
+      // LayerNorm backward folded into the next dG (reading R4 in DESIGN.md).  With u = gy + rs dn
+      // and n the normalised input of block l:  dx = u - rs (m1 + m2 n),  m1 = mean_f(dn),
+      // m2 = mean_f(dn n), so the dG GEMM of block l-1 runs on the 32-row operand [u | n] (N = 32)
+      // and its epilogue corrects per row:  dG = acc_u - rs (m1 c2_h + m2 acc_n),  c2_h = sum_k
+      // W2[k][h] (task_stream_fold).  [u | n] needs no row reduction, so the LayerNorm-backward
+      // sums overlap dG's weight stream; the exact dx (dW2 operand stash, db2 partials, residual
+      // gradient, message) is formed off the critical path.
       const int L = t.L;
-      if (own_d) {  // dY of the top block: bf16 operand + db2 column sums
+      __nv_bfloat16* const uc = t.layers[0].uc;  // [32][d] task scratch [u | n]
+      // rmu / rrs / rsb: m1, m2, rstd of the LayerNorm whose backward feeds the current dG (0 for
+      // the top block, whose dG operand is the exact incoming gradient)
+      if (et < 16) rmu[et] = rrs[et] = rsb[et] = 0.0f;
+      epi_bar();
+      // combine the LN-backward chunk sums of backward step kk (row sums of dn, dn n) -> rmu, rrs
+      auto bwd_rows = [&](int kk, int lb) {
+        const int J = d / 32;
+        const float* st = t.stats + (size_t)kk * J * 32;
+        wait_cnt(3 + 3 * kk, 4, (unsigned)J);
+        const int rr = et >> 3, jl = et & 7;
+        float s1 = 0.0f, s2 = 0.0f;
+        for (int j = jl; j < J; j += 8) {
+          const float2 v = __ldcg(reinterpret_cast<const float2*>(st + ((size_t)j * 16 + rr) * 2));
+          s1 += v.x;
+          s2 += v.y;
+        }
+        s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+        if (jl == 0) {
+          rmu[rr] = s1 / (float)d;
+          rrs[rr] = s2 / (float)d;
+          rsb[rr] = rr < M ? t.micro[lb].rstd[rr] : 0.0f;
+        }
+        epi_bar();
+      };
+      float gyv[4] = {0.f, 0.f, 0.f, 0.f};  // d-space item of the incoming gradient of the current block
+      if (own_d) {  // top block: exact dY (stash + db2 column sums), operand [gy | 0]
         const SMicro& Mi = t.micro[L - 1];
-        float g[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int r = 4 * ew + e;
-          g[e] = r < M ? __ldcg(t.gy_top + (size_t)r * d + fo) : 0.0f;
-          if (r < M) Mi.dyop[(size_t)r * d + fo] = __float2bfloat16_rn(g[e]);
+          gyv[e] = r < M ? __ldcg(t.gy_top + (size_t)r * d + fo) : 0.0f;
+          const __nv_bfloat16 gb = __float2bfloat16_rn(gyv[e]);
+          if (r < M) Mi.dyop[(size_t)r * d + fo] = gb;
+          uc[(size_t)r * d + fo] = gb;
+          uc[(size_t)(16 + r) * d + fo] = __float2bfloat16_rn(0.0f);
         }
-        colsums(g, nullptr, nullptr, Mi.pb2, nullptr, nullptr);
         signal(1, fo / (d / 4));
+        colsums(gyv, nullptr, nullptr, Mi.pb2, nullptr, nullptr);
       }
       for (int k = 0; k < L; ++k) {
         const int l = L - 1 - k;
         const SLayer& Ly = t.layers[l];
         const SMicro& Mi = t.micro[l];
         cur_p = 2 * k;
-        if (own_h) {  // dG epilogue: dA = dG * dropout mask * GELU'(a)
+        if (own_h) {  // dG epilogue: row correction, dA = dG * dropout mask * GELU'(a)
+          if (!own_d && k > 0) bwd_rows(k - 1, l + 1);
           const uint32_t dth = Ly.drop_thresh, site = Ly.site;
           const float dsc = Ly.drop_scale;
           const uint32_t step = dth ? *t.step : 0u;
+          const float c2 = Ly.c2fold[fo];
           __nv_bfloat16* const daop = Mi.daop;
           float* const pb = Mi.pb;
           float av[4];
@@ -545,14 +622,14 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             const int r = 4 * ew + e;
             av[e] = r < M ? Mi.a[(size_t)r * H + fo] : 0.0f;
           }
-          float acc[4], da[4];
-          gemm_result(acc);
+          float acc[4], accn[4], da[4];
+          gemm_result(std::integral_constant<int, 32>{}, acc, accn);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int r = 4 * ew + e;
             da[e] = 0.0f;
             if (r >= M) continue;
-            float dg = acc[e];
+            float dg = acc[e] - rsb[r] * (rmu[r] * c2 + rrs[r] * accn[e]);
             if (dth) {
               const uint64_t idx = (uint64_t)(t.r0 + r) * (uint64_t)H + (uint64_t)fo;
               dg = dropout_keep(t.seed, step, site, idx, dth) ? dg * dsc : 0.0f;
@@ -564,11 +641,9 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           colsums(da, nullptr, nullptr, pb, nullptr, nullptr);
         }
         cur_p = 2 * k + 1;
-        if (own_d) {  // dH epilogue: LayerNorm backward + residual
+        if (own_d) {  // dH epilogue: u = gy + rs dn and n for the next dG; LN-backward sums; exact dx
           const float gam = Ly.gamma[fo];
-          const float* gy = (l == L - 1) ? t.gy_top : (((l + 1) & 1) ? t.gbuf1 : t.gbuf0);
-          float* dx = (l == 0) ? t.dx_bottom : ((l & 1) ? t.gbuf1 : t.gbuf0);
-          float nv[4], gyv[4], rsv[4];
+          float nv[4], rsv[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int r = 4 * ew + e;
@@ -576,89 +651,106 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
               const float mu = Mi.mean[r];
               rsv[e] = Mi.rstd[r];
               nv[e] = (Mi.x[(size_t)r * d + fo] - mu) * rsv[e];
-              gyv[e] = __ldcg(gy + (size_t)r * d + fo);
             } else {
-              nv[e] = gyv[e] = rsv[e] = 0.0f;
+              nv[e] = rsv[e] = 0.0f;
             }
           }
           float* const pg = Mi.pg;
           float* const pbt = Mi.pbt;
           __nv_bfloat16* const dyn = l > 0 ? t.micro[l - 1].dyop : nullptr;
           float* const pb2n = l > 0 ? t.micro[l - 1].pb2 : nullptr;
-          float dh[4], dhn[4], dn[4];
-          gemm_result(dh);
+          float dh[4], dhn[4], dn[4], uv[4];
+          gemm_result(std::integral_constant<int, 16>{}, dh, nullptr);
           const int J = d / 32;
           float* st = t.stats + (size_t)k * J * 32;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            if (4 * ew + e >= M) dh[e] = 0.0f;
+            const int r = 4 * ew + e;
+            if (r >= M) dh[e] = 0.0f;
             dhn[e] = dh[e] * nv[e];
             dn[e] = dh[e] * gam;
+            uv[e] = r < M ? gyv[e] + rsv[e] * dn[e] : 0.0f;
+          }
+          if (l > 0) {  // the next dG's operand first (critical path)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int r = 4 * ew + e;
+              uc[(size_t)r * d + fo] = __float2bfloat16_rn(uv[e]);
+              uc[(size_t)(16 + r) * d + fo] = __float2bfloat16_rn(nv[e]);
+            }
+            signal(4 + 3 * k, fo / (d / 4));
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
             const float s1 = wsum32(dn[e]);
             const float s2 = wsum32(dn[e] * nv[e]);
             if (lane == 0) *reinterpret_cast<float2*>(st + ((size_t)chunk * 16 + 4 * ew + e) * 2) = make_float2(s1, s2);
           }
           signal(3 + 3 * k, 4);
           colsums(dhn, dh, nullptr, pg, pbt, nullptr);
-          wait_cnt(3 + 3 * k, 4, (unsigned)J);
-          {
-            const int rr = et >> 3, jl = et & 7;
-            float s1 = 0.0f, s2 = 0.0f;
-            for (int j = jl; j < J; j += 8) {
-              const float2 v = __ldcg(reinterpret_cast<const float2*>(st + ((size_t)j * 16 + rr) * 2));
-              s1 += v.x;
-              s2 += v.y;
-            }
-            s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
-            s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
-            s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
-            s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
-            s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
-            s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
-            if (jl == 0) {
-              rmu[rr] = s1 / (float)d;
-              rrs[rr] = s2 / (float)d;
-            }
-          }
-          epi_bar();
-          float dxv[4];
+          // exact dx = u - rs (m1 + m2 n): the next block's residual gradient and dW2 operand
+          bwd_rows(k, l);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int r = 4 * ew + e;
-            dxv[e] = 0.0f;
-            if (r >= M) continue;
-            dxv[e] = gyv[e] + rsv[e] * (dn[e] - rmu[r] - nv[e] * rrs[r]);
+            gyv[e] = r < M ? uv[e] - rsv[e] * (rmu[r] + nv[e] * rrs[r]) : 0.0f;
           }
-          if (l > 0) {  // the next block's dG operand first (critical path), then the rest
+          if (l > 0) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int r = 4 * ew + e;
-              if (r < M) dyn[(size_t)r * d + fo] = __float2bfloat16_rn(dxv[e]);
+              if (r < M) dyn[(size_t)r * d + fo] = __float2bfloat16_rn(gyv[e]);
             }
-            signal(4 + 3 * k, fo / (d / 4));
-            colsums(dxv, nullptr, nullptr, pb2n, nullptr, nullptr);
-          }
+            colsums(gyv, nullptr, nullptr, pb2n, nullptr, nullptr);
+          } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (4 * ew + e < M) dx[(size_t)(4 * ew + e) * d + fo] = dxv[e];
+            for (int e = 0; e < 4; ++e)
+              if (4 * ew + e < M) t.dx_bottom[(size_t)(4 * ew + e) * d + fo] = gyv[e];
+          }
         }
       }
     }
   }
   __syncthreads();
   cluster_sync();
-  if (warp == 1) tmem_dealloc(tmem, 32);
+  if (warp == 1) tmem_dealloc(tmem, 64);
 }
 
 // c[h] = sum_k gamma[k] W1[h][k], e[h] = sum_k beta[k] W1[h][k] + b1[h]: one warp per row, lanes
 // stride the row in 8-element vectors, fixed-order sums (deterministic)
-__global__ void __launch_bounds__(256) task_stream_fold_kernel(const __nv_bfloat16* __restrict__ W, int d, int H,
-                                                               const float* __restrict__ gamma,
-                                                               const float* __restrict__ beta,
-                                                               const float* __restrict__ b1, float* c, float* e) {
+__global__ void __launch_bounds__(256) task_stream_fold_kernel(const SLayer* __restrict__ layers, int d, int H) {
+  const SLayer& Ly = layers[blockIdx.y];
+  if (blockIdx.z == 1) {
+    // column sums of W2 [d][H], stage 1: block (row chunk kc of 256 rows, column block) -> partial
+    // sums of 8 columns per thread over the chunk's rows (fixed order) into c2part[L][d/256][H]
+    const int cb = H / (8 * 256) > 0 ? H / (8 * 256) : 1;  // column blocks of 2048 columns
+    const int kc = blockIdx.x / cb, col0 = ((blockIdx.x % cb) * 256 + threadIdx.x) * 8;
+    if (kc * 256 >= d || col0 >= H) return;
+    const __nv_bfloat16* __restrict__ W2 = Ly.w2;
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int k = kc * 256; k < kc * 256 + 256; ++k) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(W2 + (size_t)k * H + col0);
+      const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(w2[q]);
+        a[2 * q] += f.x;
+        a[2 * q + 1] += f.y;
+      }
+    }
+    float* part = Ly.c2part + (size_t)kc * H + col0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) part[q] = a[q];
+    return;
+  }
+  const __nv_bfloat16* __restrict__ W = Ly.w1;
+  const float* __restrict__ gamma = Ly.gamma;
+  const float* __restrict__ beta = Ly.beta;
   const int h = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (h >= H) return;
   float sc = 0.0f, se = 0.0f;
+#pragma unroll 4
   for (int k = lane * 8; k < d; k += 256) {
     const uint4 raw = *reinterpret_cast<const uint4*>(W + (size_t)h * d + k);
     const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
@@ -673,14 +765,24 @@ __global__ void __launch_bounds__(256) task_stream_fold_kernel(const __nv_bfloat
   sc = wsum32(sc);
   se = wsum32(se);
   if (lane == 0) {
-    c[h] = sc;
-    e[h] = se + b1[h];
+    const_cast<float*>(Ly.cfold)[h] = sc;
+    const_cast<float*>(Ly.efold)[h] = se + Ly.b1[h];
   }
 }
 
-int task_stream_fold(cudaStream_t st, const __nv_bfloat16* W1, int d, int H, const float* gamma, const float* beta,
-                     const float* b1, float* c, float* e) {
-  task_stream_fold_kernel<<<(H + 7) / 8, 256, 0, st>>>(W1, d, H, gamma, beta, b1, c, e);
+// column sums of W2, stage 2: fixed-order sum of the d/256 chunk partials
+__global__ void __launch_bounds__(256) task_stream_fold2_kernel(const SLayer* __restrict__ layers, int d, int H) {
+  const SLayer& Ly = layers[blockIdx.y];
+  const int h = blockIdx.x * 256 + threadIdx.x;
+  if (h >= H) return;
+  float acc = 0.0f;
+  for (int kc = 0; kc < d / 256; ++kc) acc += Ly.c2part[(size_t)kc * H + h];
+  const_cast<float*>(Ly.c2fold)[h] = acc;
+}
+
+int task_stream_fold(cudaStream_t st, const SLayer* layers, int L, int d, int H) {
+  task_stream_fold_kernel<<<dim3((H + 7) / 8, L, 2), 256, 0, st>>>(layers, d, H);
+  task_stream_fold2_kernel<<<dim3((H + 255) / 256, L), 256, 0, st>>>(layers, d, H);
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {
     set_error("task_stream_fold launch: %s", cudaGetErrorString(err));

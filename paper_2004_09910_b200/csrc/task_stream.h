@@ -19,6 +19,7 @@ struct alignas(64) SLayer {
   CUtensorMap dyop;  // dYop [max_batch][d] bf16, box {64, 16}  (output grad = dG operand, dW2 stash)
   CUtensorMap daop;  // dAop [max_batch][H] bf16, box {64, 16}  (pre-act grad = dH operand, dW1 stash)
   CUtensorMap ygm;   // yg [16][d] bf16, box {64, 16}: forward GEMM1 operand gamma (y - mu~) (task scratch)
+  CUtensorMap ucm;   // uc [32][d] bf16, box {64, 32}: backward dG operand [u | n] (task scratch)
   CUtensorMap w1c;   // diagnostics: W1 viewed as contiguous 16 KB tiles [H*d/64][64], box {64, 128}
   CUtensorMap w2c;   // diagnostics: W2 likewise
   const float* gamma;
@@ -27,7 +28,12 @@ struct alignas(64) SLayer {
   const float* b2;
   const float* cfold;  // [H] c_h = sum_k gamma_k W1[h][k]  (fp32 over the bf16 weights)
   const float* efold;  // [H] e_h = sum_k beta_k W1[h][k] + b1[h]
+  const float* c2fold; // [H] c2_h = sum_k W2[k][h]  (column sums of W2 [d][H])
+  float* c2part;       // [d/256][H] stage-1 partial column sums
   __nv_bfloat16* yg;   // [16][d] GEMM1 operand scratch (the memory behind ygm)
+  const __nv_bfloat16* w1;  // W1 [H][d] (for the fold kernel)
+  const __nv_bfloat16* w2;  // W2 [d][H]
+  __nv_bfloat16* uc;        // [32][d] backward dG operand scratch (the memory behind ucm)
   uint32_t drop_thresh;  // dropout after GELU: keep iff (philox word >> 8) >= thresh (0 = none)
   float drop_scale;
   uint32_t site;         // global layer index (Philox counter word 2)
@@ -74,7 +80,7 @@ int task_stream_max_clusters(int dev);
 int task_stream_launch(cudaStream_t st, const STask& t, int clusters);
 // c[h] = sum_k gamma[k] W1[h][k], e[h] = sum_k beta[k] W1[h][k] + b1[h] (fixed-order fp32 sums over
 // the bf16 weights; one warp per row)
-int task_stream_fold(cudaStream_t st, const __nv_bfloat16* W1, int d, int H, const float* gamma, const float* beta,
-                     const float* b1, float* c, float* e);
+// for all L blocks of `layers` (device array) in one launch
+int task_stream_fold(cudaStream_t st, const SLayer* layers, int L, int d, int H);
 
 }  // namespace tgp
