@@ -31,15 +31,18 @@ def main():
         layers = C.umlp(d=256, levels=2, blocks_per_level=1, mid_blocks=1)
         bal = None
     else:
-        layers = C.resmlp_stack(2 * ws, 256, dropout=0.1)
+        # "stream": d = 512, eligible for the persistent stream kernel in every partition
+        layers = C.resmlp_stack(2 * ws, 512 if cfg == "stream" else 256, dropout=0.1)
         bal = [2] * ws
-    B, m, lr, seed = 32, 4, 0.05, 11
+    B, m, lr, seed = (64 if cfg == "stream" else 32), 4, 0.05, 11
     x, t = G.inputs(layers, B, seed=seed, dtype="bf16")
     params = G.params(layers, seed=seed, dtype="bf16")
     devices = [-1] * ws
     devices[rank] = dev
     P = Pipeline(layers, chunks=m, devices=devices, balance=bal, checkpoint="except_last", max_batch=B,
                  dtype="bf16", seed=seed)
+    if cfg == "stream":
+        assert P.stream_enabled(rank), "stream kernel expected for every partition"
     connect_pipeline(P, rank, ws)
     for i in range(P.n_params):
         if P.param_info(i)[1] == rank:

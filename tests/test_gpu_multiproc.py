@@ -24,15 +24,15 @@ def _run(world, cfg, tmp_path):
     return [dict(np.load(os.path.join(tmp_path, f"rank{k}.npz"))) for k in range(world)]
 
 
-@pytest.mark.parametrize("world,cfg", [(2, "resmlp"), (4, "resmlp"), (3, "umlp")])
+@pytest.mark.parametrize("world,cfg", [(2, "resmlp"), (4, "resmlp"), (3, "umlp"), (2, "stream")])
 def test_multiprocess_matches_oracle(world, cfg, tmp_path):
     from oracle import model as OM
     res = _run(world, cfg, tmp_path)
     if cfg == "umlp":
         layers = C.umlp(d=256, levels=2, blocks_per_level=1, mid_blocks=1)
     else:
-        layers = C.resmlp_stack(2 * world, 256, dropout=0.1)
-    B, m, lr, seed = 32, 4, 0.05, 11
+        layers = C.resmlp_stack(2 * world, 512 if cfg == "stream" else 256, dropout=0.1)
+    B, m, lr, seed = (64 if cfg == "stream" else 32), 4, 0.05, 11
     x, t = G.inputs(layers, B, seed=seed, dtype="bf16")
     params = G.params(layers, seed=seed, dtype="bf16")
     ref = OM.train_step(layers, params, x, t, lr=lr, m=m, seed=seed, step=0)
