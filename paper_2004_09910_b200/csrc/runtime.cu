@@ -404,6 +404,7 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
   t.seed = c->seed;
   t.step = s.dstep;
   t.flags = c->st_flags;
+  t.sleep_ns = c->st_sleep_ns;
   if (getenv("TGP_ST_DEBUG")) {  // diagnostics: per-CTA, per-phase %globaltimer stamps
     const size_t nd = (size_t)s.st_clusters * 4 * 2 * t.L * ST_DBG_SLOTS;
     if (!s.st_dbg) {

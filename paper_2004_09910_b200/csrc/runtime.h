@@ -153,7 +153,8 @@ struct tgp_ctx {
   bool use_graphs = true, use_pdl = true, trace = false, poison = false, prefetch = false, persistent = false;
   bool l2pf = false;
   bool stream = true;
-  int st_flags = 0;  // test only: bit 0 = stream kernel ignores dependencies (timing of the bare weight stream)  // persistent weight-streaming task kernel where eligible (task_stream.cu)
+  int st_flags = 0;
+  unsigned st_sleep_ns = 32;  // stream kernel: back-off between dependency polls (option "stream_poll_ns")  // test only: bit 0 = stream kernel ignores dependencies (timing of the bare weight stream)  // persistent weight-streaming task kernel where eligible (task_stream.cu)
   int splitk = 0, skip_wait_part = -1;
   uint64_t delay_push_ns = 0;
   bool can_flush = false;

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
           rp = next_active(rp + 1);
           progress = true;
         }
-        if (!progress) __nanosleep(32);
+        if (!progress) __nanosleep(t.sleep_ns);
       }
     }
     __syncwarp();
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
     };
     auto wait_cnt = [&](int id, int q, unsigned need) {
       if (et == 0) {
-        while (!(t.flags & 1) && ld_relaxed_u32(cnt(id, q)) < need) __nanosleep(32);
+        while (!(t.flags & 1) && ld_relaxed_u32(cnt(id, q)) < need) __nanosleep(t.sleep_ns);
         fence_acq_rel_gpu();
         dbg_stamp(t, cur_p, 8);
       }

@@ -70,6 +70,7 @@ struct STask {
   // bits 0/1 make the results garbage)
   unsigned long long* dbg;
   int flags;
+  unsigned sleep_ns;  // back-off between dependency polls
 };
 constexpr int ST_DBG_SLOTS = 10;
 
