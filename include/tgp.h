@@ -179,6 +179,7 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *             pipeline depth into L2 before its grid-dependency wait (default 0)
  *  "stream"   run F / F' / B of all-RESMLP partitions with <= 16-row micro-batches as ONE persistent
  *             weight-streaming kernel per task (task_stream.cu; default 1 where eligible)
+ *  "dw_persistent" deferred weight gradients through the persistent 128x128-tile dW kernel (default 1)
  *  "stream_poll_ns" back-off of the stream kernel's dependency polling loops, ns (default 32)
  *  "persistent" run F / F' of all-RESMLP partitions (<= 16-row micro-batches) as ONE cooperative
  *             persistent kernel with grid barriers between phases (default 0)

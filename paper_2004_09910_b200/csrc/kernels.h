@@ -20,6 +20,10 @@ struct TcMat {
 //   B: b_mn == false -> memory [rows][K] (K-major, n = row, offset p.n0);  b_mn == true -> [K][N]
 //   B1: optional second K-segment (k >= p.k_seg), same majorness.
 // splits <= 0: automatic split-K (cluster size) heuristic.
+// Persistent deferred weight-gradient GEMM (gemm_dw.cu): D[M][N] (=|+=) sum_k A[k][m] B[k][n], bf16
+// operands stored [K][M] / [K][N], fp32 D; M, N multiples of 128.
+int gemm_dw(cudaStream_t st, const void* A, int64_t lda, const void* B, int64_t ldb, float* D, int64_t ldd, int M,
+            int N, int K, bool accumulate);
 int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B0, const TcMat* B1, bool b_mn,
             GemmParams p, int splits);
 // 2-D bf16 TMA descriptor over a row-major matrix, 128-byte swizzle, box {box_inner, box_outer}.
@@ -69,6 +73,13 @@ int act_bwd_rows(cudaStream_t st, bool pdl, const float* dy, const float* z, int
 int add_rows(cudaStream_t st, bool pdl, float* y, const float* a, int64_t n);
 // sum over m partial rows [m][d] in fixed order -> out[d] (=|+=)
 int reduce_partials(cudaStream_t st, const float* part, int m, int d, float* out, bool accumulate);
+struct RedItem {
+  const float* part;  // [m][d] per-micro-batch column partials
+  float* out;         // [d] gradient
+  int d;
+  int pad;
+};
+int reduce_partials_multi(cudaStream_t st, const RedItem* items, int n_items, int max_d, int m, bool accumulate);
 // MSE loss + gradient: loss = sum (y-t)^2 / n_total; dy = 2 (y-t) / n_total. Deterministic.
 int mse_loss_grad(cudaStream_t st, const float* y, const float* t, int64_t n, float* dy, double* loss_dev);
 // SGD: master -= lr * grad; shadow (bf16, nullable) = bf16(master)

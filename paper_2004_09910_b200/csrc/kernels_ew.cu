@@ -229,6 +229,21 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part, int m, in
   for (int i = 0; i < m; ++i) s += part[(int64_t)i * d + c];
   out[c] = acc ? out[c] + s : s;
 }
+// all column-partial reductions of a partition in one launch: item blockIdx.y reduces its [m][d]
+// partial rows into out (fixed row order per column, as reduce_partials_kernel)
+__global__ void reduce_partials_multi_kernel(const RedItem* __restrict__ items, int m, int acc) {
+  const RedItem it = items[blockIdx.y];
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= it.d) return;
+  float s = 0.0f;
+#pragma unroll 8
+  for (int i = 0; i < m; ++i) s += it.part[(int64_t)i * it.d + c];
+  it.out[c] = acc ? it.out[c] + s : s;
+}
+int reduce_partials_multi(cudaStream_t st, const RedItem* items, int n_items, int max_d, int m, bool accumulate) {
+  return launch("reduce_partials_multi", reduce_partials_multi_kernel, dim3((max_d + 255) / 256, n_items), dim3(256),
+                st, false, items, m, (int)accumulate);
+}
 int reduce_partials(cudaStream_t st, const float* part, int m, int d, float* out, bool accumulate) {
   return launch("reduce_partials", reduce_partials_kernel, dim3((d + 255) / 256), dim3(256), st, false, part, m, d,
                 out, (int)accumulate);

@@ -178,6 +178,8 @@ static int run_gemm(tgp_ctx* c, Stage& s, bool pdl, Opnd A, bool a_mn, Opnd B0, 
       set_error("merge: d_in=%d must be a multiple of 64 in bf16 mode", k_seg);
       return TGP_E_UNSUPPORTED;
     }
+    if (e.mode == EPI_DW && a_mn && b_mn && !B1 && M % 128 == 0 && N % 128 == 0 && c->dw_persistent)
+      return gemm_dw(s.comp, A.p, A.ld, B0.p, B0.ld, e.dw, e.ldw, M, N, K, e.accumulate != 0);
     return gemm_tc(s.comp, pdl && c->use_pdl, a, a_mn, b0, B1 ? &b1 : nullptr, b_mn, p, c->splitk);
   }
   SimtOperand sa = a_mn ? SimtOperand{(const float*)A.p, 1, A.ld} : SimtOperand{(const float*)A.p, A.ld, 1};
@@ -670,8 +672,6 @@ static int exec_wgrad(tgp_ctx* c, Stage& s, int B) {
           TGP_TRY(run_gemm(c, s, false, Opnd{L.Zop, B, dout, dout}, true, Opnd{s.self.skip_in[R.id], B, R.width, R.width},
                            nullptr, true, dout, R.width, B, 0, B, false, e));
         }
-        TGP_TRY(reduce_partials(s.comp, L.pb, c->m * c->pb, dout, gparam(s, L, 1), acc));
-        c->kernels++;
         break;
       }
       case TGP_RESMLP: {
@@ -684,20 +684,16 @@ static int exec_wgrad(tgp_ctx* c, Stage& s, int B) {
         e.ldw = H;
         TGP_TRY(run_gemm(c, s, false, Opnd{L.dYop, B, dout, dout}, true, Opnd{L.Gop, B, H, H}, nullptr, true, dout, H, B,
                          0, B, false, e));
-        TGP_TRY(reduce_partials(s.comp, L.pg, c->m * c->pb, din, gparam(s, L, 0), acc));
-        TGP_TRY(reduce_partials(s.comp, L.pbt, c->m * c->pb, din, gparam(s, L, 1), acc));
-        TGP_TRY(reduce_partials(s.comp, L.pb, c->m * c->pb, H, gparam(s, L, 3), acc));
-        TGP_TRY(reduce_partials(s.comp, L.pb2, c->m * c->pb, dout, gparam(s, L, 5), acc));
-        c->kernels += 4;
         break;
       }
-      case TGP_BATCHNORM: {
-        TGP_TRY(reduce_partials(s.comp, L.pg, c->m * c->pb, din, gparam(s, L, 0), acc));
-        TGP_TRY(reduce_partials(s.comp, L.pb, c->m * c->pb, din, gparam(s, L, 1), acc));
-        c->kernels += 2;
+      case TGP_BATCHNORM:
         break;
-      }
     }
+  }
+  // every bias / LayerNorm / BatchNorm column-partial reduction of the partition in one launch
+  if (s.n_red > 0) {
+    TGP_TRY(reduce_partials_multi(s.comp, (const RedItem*)s.red_items, s.n_red, s.red_maxd, c->m * c->pb, acc));
+    c->kernels++;
   }
   s.grads_fresh = false;
   return 0;

@@ -115,6 +115,8 @@ struct Stage {
   float* st_c2part = nullptr; // [L][d/256][H] partial column sums of W2
   bool fold_dirty = true;     // weights / LN parameters changed since st_fold was computed
   unsigned long long* st_dbg = nullptr;  // diagnostics (TGP_ST_DEBUG): [grid][2L][ST_DBG_SLOTS]
+  void* red_items = nullptr;  // device RedItem[n_red]: column-partial -> gradient reductions of W_j
+  int n_red = 0, red_maxd = 0;
   std::vector<TaskGraph> gF, gB;
   TaskGraph gW;
   bool grads_fresh = true;
@@ -154,6 +156,7 @@ struct tgp_ctx {
   bool l2pf = false;
   bool stream = true;
   int st_flags = 0;
+  bool dw_persistent = true;  // deferred dW through the persistent gemm_dw kernel (option "dw_persistent")
   unsigned st_sleep_ns = 32;  // stream kernel: back-off between dependency polls (option "stream_poll_ns")  // test only: bit 0 = stream kernel ignores dependencies (timing of the bare weight stream)  // persistent weight-streaming task kernel where eligible (task_stream.cu)
   int splitk = 0, skip_wait_part = -1;
   uint64_t delay_push_ns = 0;
