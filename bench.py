@@ -132,7 +132,9 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    v, cores, desc = cpu_oracle_sample(steps=max(1, args.steps), blocks=args.ref_blocks)
+    # each step a bounded sample (2 of the 32 blocks at full width and batch, ~7 s on 16 cores) so a
+    # --steps K run of the reference arm stays within a few minutes
+    v, cores, desc = cpu_oracle_sample(steps=max(1, args.steps), blocks=min(args.ref_blocks, 2))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH / v,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
