@@ -144,10 +144,10 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def _config(n):
+def _config(n, m=M_CHUNKS, ckpt="except_last"):
     return {"workload": f"C2: {BLOCKS}-block pre-LN residual MLP (width {WIDTH}, GELU, LayerNorm), global batch "
-                        f"{BATCH}, m={M_CHUNKS}, checkpoint=except_last, plain SGD, MSE",
-            "global_batch": BATCH, "micro_batch_rows": BATCH // M_CHUNKS, "chunks": M_CHUNKS, "partitions": n,
+                        f"{BATCH}, m={m}, checkpoint={ckpt}, plain SGD, MSE",
+            "global_batch": BATCH, "micro_batch_rows": BATCH // m, "chunks": m, "checkpoint": ckpt, "partitions": n,
             "parallelism": f"pp{n}", "seq_len": None,
             "l2": "no flush: 2.15 GB of bf16 weights streamed per step exceed the 126 MB L2"}
 
@@ -170,7 +170,7 @@ def run_tgp(args):
     layers = C.resmlp_stack(BLOCKS, WIDTH)
     devices = [-1] * n
     devices[rank] = lrank
-    P = Pipeline(layers, chunks=M_CHUNKS, devices=devices, balance=[BLOCKS // n] * n, checkpoint=args.checkpoint,
+    P = Pipeline(layers, chunks=args.chunks, devices=devices, balance=[BLOCKS // n] * n, checkpoint=args.checkpoint,
                  max_batch=BATCH, dtype="bf16", seed=1234)
     if ws > 1:
         from paper_2004_09910_b200.dist import connect_pipeline
@@ -261,7 +261,7 @@ def run_tgp(args):
             "metric": METRIC, "value": sps, "unit": UNIT, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (N(0,1) inputs/targets, on-device U(+-1/sqrt(fan_in)) init)",
-            "config": _config(n),
+            "config": _config(n, args.chunks, args.checkpoint),
             "e2e": {"value": BATCH * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": 4 * BATCH * WIDTH * 2, "d2h_bytes_per_step": 8},
             "gpu_launches": int(nk),
@@ -287,6 +287,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="tgp", choices=["tgp", "reference"])
     ap.add_argument("--checkpoint", default="except_last", choices=["always", "except_last", "never"])
+    ap.add_argument("--chunks", type=int, default=M_CHUNKS, help="m (BASELINE metric: 32; other values = C3 sweep)")
     ap.add_argument("--lr", type=float, default=0.05)
     ap.add_argument("--ref-blocks", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -181,8 +181,6 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *             weight-streaming kernel per task (task_stream.cu; default 1 where eligible)
  *  "dw_persistent" deferred weight gradients through the persistent 128x128-tile dW kernel (default 1)
  *  "stream_poll_ns" back-off of the stream kernel's dependency polling loops, ns (default 32)
- *  "persistent" run F / F' of all-RESMLP partitions (<= 16-row micro-batches) as ONE cooperative
- *             persistent kernel with grid barriers between phases (default 0)
  * Test-only negative controls (never used on the product path):
  *  "test_poison"        fill the forward receive slabs with NaN before each forward call
  *  "test_skip_wait"     drop the receive waits of partition `value` (-1 = none)
@@ -208,11 +206,6 @@ tgp_status tgp_bench_dominant_gemm(tgp_ctx* ctx, int32_t part, int32_t B, int32_
  * kernel (F_{1,j} launches: *bytes = its algorithmic bytes -- weights plus activations read and
  * written once) instead of the per-layer forward GEMM. */
 tgp_status tgp_stream_enabled(tgp_ctx* ctx, int32_t part, int32_t* on);
-
-/* Diagnostics of the persistent forward-task kernel (only when the process runs with TGP_PT_DEBUG
- * set): per CTA and grid-barrier id k < 256, the %globaltimer at its arrival and release, as
- * [grid][256][2] uint64.  out may be NULL to query *n. */
-tgp_status tgp_debug_pt_read(tgp_ctx* ctx, int32_t part, uint64_t* out, int64_t cap, int64_t* n);
 
 /* Diagnostics of the persistent weight-streaming task kernel (only when the process runs with
  * TGP_ST_DEBUG set): per CTA and GEMM phase of the last task launched on partition `part`, 10

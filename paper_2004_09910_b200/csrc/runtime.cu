@@ -14,7 +14,6 @@
 
 #include "host.h"
 #include "runtime.h"
-#include "task_fwd.h"
 #include "task_stream.h"
 
 using namespace tgp;
@@ -231,75 +230,6 @@ static Prefetch next_bwd(tgp_ctx* c, Stage& s, int l) {  // after the last GEMM 
 // ============================================================================ task executors
 static void micro_rows(const tgp_ctx* c, int B, int i, int* r0, int* M);
 
-// Persistent forward task (task_fwd.cu): per-micro-batch device descriptors, (re)built when the batch
-// size changes.
-static int pt_build_desc(tgp_ctx* c, Stage& s, int B) {
-  const int L = s.l1 - s.l0;
-  std::vector<PLayer> h((size_t)c->m * L);
-  for (int i = 1; i <= c->m; ++i) {
-    int r0 = 0, M = 0;
-    micro_rows(c, B, i, &r0, &M);
-    const int slot = c->slot_of[i];
-    for (int l = s.l0; l < s.l1; ++l) {
-      LayerRT& Ly = c->layers[l];
-      const int d = Ly.L.d_in, H = Ly.L.d_hidden;
-      PLayer& P = h[(size_t)(i - 1) * L + (l - s.l0)];
-      memset(&P, 0, sizeof(P));
-      if (!make_map(&P.tmW1, TcMat{wparam(c, s, Ly, 2), H, d, d}, 64, 128) ||
-          !make_map(&P.tmW2, TcMat{wparam(c, s, Ly, 4), d, H, H}, 64, 128) ||
-          !make_map(&P.tmH, TcMat{Ly.Hop, c->max_batch, d, d}, 64, 16) ||
-          !make_map(&P.tmG, TcMat{Ly.Gop, c->max_batch, H, H}, 64, 16))
-        return TGP_E_CUDA;
-      P.gamma = mparam(s, Ly, 0);
-      P.beta = mparam(s, Ly, 1);
-      P.b1 = mparam(s, Ly, 3);
-      P.b2 = mparam(s, Ly, 5);
-      P.x = (l == s.l0) ? s.self.fwd_in + (size_t)r0 * d : c->layers[l - 1].out[slot];
-      P.y = (l == s.l1 - 1) ? s.out + (size_t)r0 * d : Ly.out[slot];
-      P.a = Ly.z[slot];
-      P.hop = (__nv_bfloat16*)opptr(c, Ly.Hop, r0, d);
-      P.gop = (__nv_bfloat16*)opptr(c, Ly.Gop, r0, H);
-      P.mean = Ly.mean[slot];
-      P.rstd = Ly.rstd[slot];
-      P.drop_thresh = drop_thresh(Ly.L.dropout);
-      P.drop_scale = Ly.L.dropout > 0 ? 1.0f / (1.0f - Ly.L.dropout) : 1.0f;
-      P.site = (uint32_t)l;
-    }
-  }
-  TGP_CUDA_TRY(cudaMemcpyAsync(s.pt_desc, h.data(), h.size() * sizeof(PLayer), cudaMemcpyHostToDevice, s.comp));
-  TGP_CUDA_TRY(cudaStreamSynchronize(s.comp));
-  s.pt_desc_B = B;
-  return 0;
-}
-
-static int exec_forward_persistent(tgp_ctx* c, Stage& s, int i, int r0, int M) {
-  const LayerRT& L0 = c->layers[s.l0];
-  PTask t{};
-  t.L = s.l1 - s.l0;
-  t.layers = (const PLayer*)s.pt_desc + (size_t)(i - 1) * t.L;
-  t.d = L0.L.d_in;
-  t.H = L0.L.d_hidden;
-  t.M = M;
-  t.r0 = r0;
-  t.ws = s.pt_ws;
-  t.ws_stride = s.pt_ws_stride;
-  t.segmax = s.pt_segmax;
-  t.stats = s.pt_stats;
-  t.bar = s.pt_bar;
-  t.seed = c->seed;
-  t.step = s.dstep;
-  if (getenv("TGP_PT_DEBUG")) {  // diagnostics: per-CTA barrier arrive / release timestamps
-    if (!s.pt_dbg) {
-      const size_t n = (size_t)s.pt_grid * 256 * 2 + 256 + (size_t)s.pt_grid * 128 * 8;
-      TGP_CUDA_TRY(cudaMalloc(&s.pt_dbg, n * 8));
-      TGP_CUDA_TRY(cudaMemset(s.pt_dbg, 0, n * 8));
-    }
-    t.dbg = (unsigned long long*)s.pt_dbg;
-  }
-  c->kernels++;
-  return task_fwd_launch(s.comp, t, s.pt_grid);
-}
-
 // Persistent weight-streaming task kernel (task_stream.cu): layer descriptors (tensor maps of the
 // weights and operand stashes) and per-(micro-batch, block) pointers, (re)built when B changes.
 static int st_build_desc(tgp_ctx* c, Stage& s, int B) {
@@ -422,7 +352,6 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
 // F_{i,j} (and F'_{i,j}: identical kernels and launch configuration -> bitwise identical output)
 static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
   if (use_stream(c, s, M)) return exec_task_stream(c, s, i, r0, M, false);
-  if (s.pt_ok && c->persistent && M <= 16) return exec_forward_persistent(c, s, i, r0, M);
   const int slot = c->slot_of[i];
   float* x = s.self.fwd_in + (size_t)r0 * s.d_in;
   bool first_kernel = true;
@@ -862,7 +791,6 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
         TGP_TRY(run_task(c, s, s.gB[i - 1], B, [&] { return exec_backward(c, s, i, r0, M); }));
         TGP_CUDA_TRY(cudaEventRecord(s.bdone[i - 1], s.comp));
       } else {
-        if (s.pt_ok && c->persistent && s.pt_desc_B != B) TGP_TRY(pt_build_desc(c, s, B));
         TGP_TRY(run_task(c, s, s.gF[i - 1], B, [&] { return exec_forward(c, s, i, r0, M); }));
         if (rc.kind == K_F) TGP_CUDA_TRY(cudaEventRecord(s.fdone[i - 1], s.comp));
       }

@@ -90,17 +90,6 @@ struct Stage {
   double* loss_buf = nullptr;
   int* bn_rows = nullptr;
   uint32_t* dstep = nullptr;  // device copy of the optimizer step (dropout counter)
-  // persistent forward-task kernel (task_fwd.cu): eligibility, per-micro-batch descriptors, workspace
-  bool pt_ok = false;
-  void* pt_desc = nullptr;  // device PLayer[m][L]
-  int pt_desc_B = -1;
-  float* pt_ws = nullptr;
-  int64_t pt_ws_stride = 0;
-  int pt_segmax = 0;
-  float* pt_stats = nullptr;
-  unsigned* pt_bar = nullptr;
-  int pt_grid = 0;
-  void* pt_dbg = nullptr;
   // persistent weight-streaming task kernel (task_stream.cu): F / F' / B of all-RESMLP partitions
   bool st_ok = false;
   int st_clusters = 0;
@@ -150,9 +139,7 @@ struct tgp_ctx {
   std::vector<int> slot_of;  // 1-based micro-batch -> slot
   int64_t kernels = 0;
   // options
-  // persistent forward-task kernel: opt-in (measured 0.93 ms vs 0.86 ms per F task at C2 n = 1;
-  // five ~2 us grid barriers per block dominate -- profiles/pt_phases.py)
-  bool use_graphs = true, use_pdl = true, trace = false, poison = false, prefetch = false, persistent = false;
+  bool use_graphs = true, use_pdl = true, trace = false, poison = false, prefetch = false;
   bool l2pf = false;
   bool stream = true;
   int st_flags = 0;

@@ -66,7 +66,6 @@ _SIGS = {
     "tgp_last_error": [],
     "tgp_bench_dominant_gemm": [_P, _I32, _I32, _I32, ctypes.POINTER(ctypes.c_double),
                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)],
-    "tgp_debug_pt_read": [_P, _I32, _P, _I64, ctypes.POINTER(_I64)],
     "tgp_debug_stream_read": [_P, _I32, _P, _I64, ctypes.POINTER(_I64)],
     "tgp_stream_enabled": [_P, _I32, ctypes.POINTER(_I32)],
     "tgp_test_gemm_bf16": [_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P],
