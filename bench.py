@@ -237,8 +237,9 @@ def run_tgp(args):
     # per block, weights streamed from HBM), timed live on the partition's compute stream
     stream = P.stream_enabled(rank)
     gemm_ms, gemm_bytes, gemm_n = P.bench_dominant_gemm(rank, BATCH, reps=10 if stream else 3)
-    kname = (f"task_stream_kernel F task ({BLOCKS // n} blocks x 2 weight-streaming GEMMs, M=16 rows, d=H={WIDTH})"
-             if stream else "gemm_tc_kernel<16> forward W1 GEMM (M=16 rows, K=N=4096)")
+    mrows = BATCH // args.chunks
+    kname = (f"task_stream_kernel F task ({BLOCKS // n} blocks x 2 weight-streaming GEMMs, M={mrows} rows, d=H={WIDTH})"
+             if stream else f"gemm_tc_kernel forward W1 GEMM (M={mrows} rows, K=N={WIDTH})")
     peaks = _peaks()
     if peaks and "hbm_gbs" in peaks:
         peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
