@@ -300,13 +300,14 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
     const int chunk = slab * SK + rank;  // 32-feature chunk index of the owner slice
     int n = 0, cur_p = 0;
     auto epi_bar = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+    // stamps (diagnostics) only for the phase's operand signal, not the statistics signals (q == 4)
     auto signal = [&](int id, int q) {
-      if (et == 0) dbg_stamp(t, cur_p, 9);
+      if (et == 0 && q < 4) dbg_stamp(t, cur_p, 9);
       epi_bar();
       if (et == 0) {
         // release: the epilogue barrier orders the other threads' stores before this reduction
         asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(cnt(id, q)), "r"(1u) : "memory");
-        dbg_stamp(t, cur_p, 7);
+        if (q < 4) dbg_stamp(t, cur_p, 7);
       }
     };
     auto wait_cnt = [&](int id, int q, unsigned need) {
