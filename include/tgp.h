@@ -219,7 +219,9 @@ tgp_status tgp_debug_stream_read(tgp_ctx* ctx, int32_t part, uint64_t* out, int6
 /* D[m][n] = sum_k A[m][k] B[n][k] on the tcgen05 path (bf16 in, fp32 out).
  * a_mn: A stored [K][M] (else [M][K]); b_mn: B stored [K][N] (else [N][K]).
  * D layout: b_mn == 1 -> row-major [M][N] (the weight-gradient orientation); b_mn == 0 -> [N][M]
- * (activation orientation: row n, feature m -- the swap-AB skinny path).  splits: split-K
+ * (activation orientation: row n, feature m -- the swap-AB skinny path).  a_mn = b_mn = 1 with
+ * splits = -1 (-2) runs the persistent deferred-dW kernel storing (accumulating) into D instead
+ * (M, N multiples of 128).  splits: split-K
  * cluster size (0 = auto).  Device pointers; stream = cudaStream_t or NULL; synchronous.  Used by
  * the kernel unit tests and micro-benchmarks. */
 tgp_status tgp_test_gemm_bf16(const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,

@@ -13,7 +13,7 @@ def _mk(shape, seed):
     return round_bf16(np.random.default_rng(seed).standard_normal(shape).astype(np.float32))
 
 
-def _run(M, N, K, a_mn, b_mn, splits=0, seed=0, reps=1):
+def _run(M, N, K, a_mn, b_mn, splits=0, seed=0, reps=1, init=None):
     import torch
 
     from paper_2004_09910_b200.tgp import test_gemm_bf16
@@ -27,7 +27,8 @@ def _run(M, N, K, a_mn, b_mn, splits=0, seed=0, reps=1):
     dB = torch.tensor(b_mem, device="cuda").to(torch.bfloat16)
     outs = []
     for _ in range(reps):
-        D = torch.full((M * N,), float("nan"), device="cuda")
+        D = torch.full((M * N,), float("nan"), device="cuda") if init is None else \
+            torch.tensor(init.ravel(), dtype=torch.float32, device="cuda")
         test_gemm_bf16(dA, dB, D, M, N, K, a_mn, b_mn, splits)
         d = D.cpu().numpy().astype(np.float64)
         d = d.reshape(M, N) if b_mn else d.reshape(N, M).T
@@ -62,3 +63,15 @@ def test_gemm_split_k_deterministic():
     # fixed-order DSMEM reduction: repeated runs are bitwise identical (reading Z21)
     outs, ref = _run(2048, 16, 4096, False, False, splits=8, reps=3)
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (4096, 4096, 512), (512, 384, 192), (1024, 2048, 256), (256, 128, 40)])
+def test_gemm_dw_persistent(M, N, K):
+    # the persistent deferred-dW kernel (W_j): store, then accumulate (TMA reduce-add) into the result
+    outs, ref = _run(M, N, K, True, True, splits=-1)
+    d = outs[0]
+    assert np.isfinite(d).all()
+    assert np.max(np.abs(d - ref)) / np.max(np.abs(ref)) <= 1e-5
+    init = np.random.default_rng(3).standard_normal((M, N)).astype(np.float32)
+    outs2, _ = _run(M, N, K, True, True, splits=-2, init=init)
+    assert np.max(np.abs(outs2[0] - (ref + init))) / np.max(np.abs(ref + init)) <= 1e-5
