@@ -39,6 +39,9 @@ def _compile(src):
     obj = os.path.join(OBJ, src + "." + _deps_hash(src) + ".o")
     if os.path.exists(obj):
         return obj
+    for f in os.listdir(OBJ):  # drop stale objects of this source
+        if f.startswith(src + ".") and f.endswith(".o"):
+            os.remove(os.path.join(OBJ, f))
     cmd = [NVCC] + ARCH + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
