@@ -56,7 +56,7 @@ constexpr int ST_A = 16384;                 // 128 x 64 bf16 weight tile
 constexpr int ST_STAGES_MAX = 11;
 constexpr int ST_LAYOUT_FWD = 11 * (ST_A + 2048) + 2 * (SK * 32 * 16 * 4);
 constexpr int ST_LAYOUT_BWD = 9 * (ST_A + 4096) + 2 * (SK * 32 * 32 * 4);
-constexpr int ST_SMEM = (ST_LAYOUT_FWD > ST_LAYOUT_BWD ? ST_LAYOUT_FWD : ST_LAYOUT_BWD) + 3072 + 1024;
+constexpr int ST_SMEM = (ST_LAYOUT_FWD > ST_LAYOUT_BWD ? ST_LAYOUT_FWD : ST_LAYOUT_BWD) + 3200 + 1024;
 constexpr int CNT_STRIDE = 32;              // uints between counters (one 128-byte line each)
 }  // namespace
 
@@ -71,6 +71,14 @@ TGP_DEV uint64_t policy_evict_normal() {
   return p;
 }
 TGP_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+TGP_DEV void st_release_cta_u32(uint32_t saddr, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+TGP_DEV uint32_t ld_acquire_cta_u32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+  return v;
+}
 TGP_DEV void dbg_stamp(const STask& t, int p, int slot) {
   if (!t.dbg) return;
   unsigned long long v;
@@ -99,7 +107,7 @@ TGP_DEV Ph phase_of(const STask& t, int p) {
   return sub ? Ph{&Ly.w1m, &Ly.daop, t.H, t.d} : Ph{&Ly.w2m, &Ly.ucm, t.d, t.H};
 }
 
-__global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_constant__ STask t) {
+__global__ void __launch_bounds__(224, 1) task_stream_kernel(const __grid_constant__ STask t) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NST = t.bwd ? 9 : 11;                   // ring depth (divisions below use literals)
@@ -131,6 +139,9 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
   // phase index of the k-th active phase of this CTA (NP if none), from a table built at start
   uint16_t* act_list = reinterpret_cast<uint16_t*>(smem + OFF_BAR + 2560);  // [<= 256]
   auto nth_active = [&](int k) { return k < NP ? (int)act_list[k] : NP; };
+  // phases < *released have their activation dependency met (written by the poller warp with
+  // st.release.cta after its gpu-scope acquire; read by the producer with ld.acquire.cta)
+  const uint32_t released = smem_u32(smem + OFF_BAR + 3072);
   auto recv_bytes = [&](int p) { return (uint32_t)(SK * 32 * ncol(p) * 4); };
   auto cnt = [&](int id, int q) { return t.cnt + ((size_t)id * 5 + q) * CNT_STRIDE; };
 
@@ -139,6 +150,7 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
     for (int p = 0; p < NP; ++p)
       if (active(p)) act_list[na++] = (uint16_t)p;
     for (int k = na; k < NP; ++k) act_list[k] = (uint16_t)NP;
+    st_release_cta_u32(released, 0u);
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -204,12 +216,8 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
       for (int q = 0; q < NST + pfd && pfd > 0; ++q) prefetch_next();
       while (wp < NP || rp < NP) {
         bool progress = false;
-        // poll the dependency of phase rp (issued first, used after the weight loop)
-        unsigned have = 0, need = 0;
-        if (rp < NP) {
-          need = (unsigned)(phase_of(t, rp).K / 128);
-          have = (t.flags & 1) ? need : ld_relaxed_u32(cnt(1 + 3 * (rp >> 1) + (rp & 1), rank));
-        }
+        // dependency of phase rp: polled by warp 6 (a global poll here would stall this loop for an
+        // L2 round trip per iteration and throttle the ring refill)
         while (wp < NP) {  // weights: run ahead as far as the ring allows
           const int s = t.bwd ? it % 9 : it % 11, r = t.bwd ? it / 9 : it / 11;
           if (!mbar_test_wait(smem_u32(&empty[s]), (uint32_t)((r & 1) ^ 1))) break;
@@ -240,9 +248,8 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
             wp = next_active(wp + 1);
           }
         }
-        if (rp < NP && have >= need) {
+        if (rp < NP && (int)ld_acquire_cta_u32(released) > rp) {
           // release phase rp: activation tiles for its k-blocks already in the ring
-          fence_acq_rel_gpu();
           asm volatile("fence.proxy.async.global;" ::: "memory");
           dbg_stamp(t, rp, 0);
           const int nkb = phase_of(t, rp).K / (SK * 64);
@@ -289,6 +296,22 @@ __global__ void __launch_bounds__(192, 1) task_stream_kernel(const __grid_consta
         dbg_stamp(t, p, 4);
         tc_commit(&tfull[buf]);
         ++n;
+      }
+    }
+    __syncwarp();
+  } else if (warp == 6) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ dependency poller
+      // for every active phase in order: wait for its activation-operand counter, then publish
+      for (int k = 0; k < NP; ++k) {
+        const int p = nth_active(k);
+        if (p >= NP) break;
+        const unsigned need = (unsigned)(phase_of(t, p).K / 128);
+        const unsigned* dep = cnt(1 + 3 * (p >> 1) + (p & 1), rank);
+        if (!(t.flags & 1))
+          while (ld_relaxed_u32(dep) < need) __nanosleep(t.sleep_ns);
+        fence_acq_rel_gpu();
+        st_release_cta_u32(released, (uint32_t)(p + 1));
       }
     }
     __syncwarp();
@@ -813,7 +836,7 @@ static bool stream_attr() {
 static void stream_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, int clusters, cudaStream_t st) {
   cfg = cudaLaunchConfig_t{};
   cfg.gridDim = dim3(clusters * SK, 1, 1);
-  cfg.blockDim = dim3(192, 1, 1);
+  cfg.blockDim = dim3(224, 1, 1);
   cfg.dynamicSmemBytes = ST_SMEM;
   cfg.stream = st;
   at[0].id = cudaLaunchAttributeClusterDimension;
