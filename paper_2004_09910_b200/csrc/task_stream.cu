@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(224, 1) task_stream_kernel(const __grid_consta
       };
       int wp = next_active(0), wkb = 0, it = 0;  // weight cursor: phase, k-block, ring tile
       int rp = next_active(0), rt0 = 0;          // lowest phase whose activations are not released; its first tile
+      int pf_phase = -1;                         // phase whose remaining tiles were L2-prefetched
       auto load_b = [&](int p, int kb, int tile) {
         const Ph P = phase_of(t, p);
         const int nkb = P.K / (SK * 64);
@@ -218,9 +219,13 @@ __global__ void __launch_bounds__(224, 1) task_stream_kernel(const __grid_consta
         bool progress = false;
         // dependency of phase rp: polled by warp 6 (a global poll here would stall this loop for an
         // L2 round trip per iteration and throttle the ring refill)
+        bool ring_full = false;
         while (wp < NP) {  // weights: run ahead as far as the ring allows
           const int s = t.bwd ? it % 9 : it % 11, r = t.bwd ? it / 9 : it / 11;
-          if (!mbar_test_wait(smem_u32(&empty[s]), (uint32_t)((r & 1) ^ 1))) break;
+          if (!mbar_test_wait(smem_u32(&empty[s]), (uint32_t)((r & 1) ^ 1))) {
+            ring_full = true;
+            break;
+          }
           const Ph P = phase_of(t, wp);
           const int nkb = P.K / (SK * 64);
           const int kc = (rank * nkb + wkb) * 64;
@@ -246,6 +251,22 @@ __global__ void __launch_bounds__(224, 1) task_stream_kernel(const __grid_consta
           if (++wkb == nkb) {
             wkb = 0;
             wp = next_active(wp + 1);
+          }
+        }
+        if (ring_full && (t.flags & 4096) && wp != pf_phase) {
+          // the ring is full: prefetch the rest of the current phase's weight tiles into L2 so they
+          // arrive from L2 once the ring drains (variant bit 12)
+          pf_phase = wp;
+          const Ph P = phase_of(t, wp);
+          const int nkb = P.K / (SK * 64);
+          for (int q = wkb; q < nkb; ++q) {
+            const int kc = (rank * nkb + q) * 64;
+            if (!t.bwd) {
+              tma_prefetch_l2_2d(P.A, kc, slab * 128);
+            } else {
+              tma_prefetch_l2_2d(P.A, slab * 128, kc);
+              tma_prefetch_l2_2d(P.A, slab * 128 + 64, kc);
+            }
           }
         }
         if (rp < NP && (int)ld_acquire_cta_u32(released) > rp) {
