@@ -33,15 +33,18 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
   uint8_t* a = sm;
   uint8_t* b = sm + 16384;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 16384 + 2048);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 4);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
     mbar_init(&bar[3], 1);
+    for (int q = 4; q < 8; ++q) mbar_init(&bar[q], 1000);
+    for (int q = 8; q < 16; ++q) mbar_init(&bar[q], 1);
     fence_barrier_init();
   }
+  if (threadIdx.x == 0) slot[2] = 1;
   if (warp == 0) tmem_alloc(slot, 128);
   tc_fence_before();
   __syncthreads();
@@ -94,6 +97,19 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
       long long t1 = clock64();
       dss[16 * 128 + 3] = (float)(t1 - t0);
     }
+    for (int variant = 0; variant < 2; ++variant) {
+      const int every = variant ? 16 : 4;
+      long long t0 = clock64();
+      for (int i = 0; i < 64; ++i) {
+        const int kk = i & 3;
+        tc_mma_bf16(tmem + 32, make_sdesc_sw128(sa + kk * 32, 16, 1024), make_sdesc_sw128(sb + kk * 32, 16, 1024), idesc, 1);
+        if ((i + 1) % every == 0) tc_commit(&bar[4 + ((i / every) & 3)]);
+      }
+      tc_commit(&bar[8 + variant]);
+      mbar_wait(&bar[8 + variant], 0);
+      long long t1 = clock64();
+      dss[16 * 128 + 5 + variant] = (float)(t1 - t0);
+    }
     {
       const uint32_t idesc64 = make_idesc_bf16(128, 64, false, false);
       long long t0 = clock64();
@@ -118,6 +134,69 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
     }
   }
   __syncwarp();
+  __syncthreads();
+  // two issuing warps, 32 MMAs each into different accumulators, concurrently
+  {
+    const uint32_t idesc = make_idesc_bf16(128, 16, false, false);
+    const uint32_t sa = smem_u32(a), sb = smem_u32(b);
+    if ((threadIdx.x == 0 || threadIdx.x == 32)) {
+      const int w = threadIdx.x >> 5;
+      long long t0 = clock64();
+      for (int i = 0; i < 32; ++i) {
+        const int kk = i & 3;
+        tc_mma_bf16(tmem + 32 + w * 16, make_sdesc_sw128(sa + kk * 32, 16, 1024), make_sdesc_sw128(sb + kk * 32, 16, 1024),
+                    idesc, 1);
+      }
+      tc_commit(&bar[8 + w]);
+      mbar_wait(&bar[8 + w], 1);
+      long long t1 = clock64();
+      dss[16 * 128 + 7 + w] = (float)(t1 - t0);
+    }
+  }
+  __syncthreads();
+  // "tile loop" as in the stream kernel: per tile test_wait(complete barrier) + fence + 4 MMAs + commit
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc_bf16(128, 16, false, false);
+    const uint32_t sa = smem_u32(a), sb = smem_u32(b);
+    for (int variant = 0; variant < 6; ++variant) {
+      long long t0 = clock64();
+      if (variant >= 4) {  // batched: per group of 4 tiles, the waits first, then 16 MMAs, then 4 commits
+        for (int gi = 0; gi < 4; ++gi) {
+          for (int q = 0; q < (variant == 4 ? 4 : 1); ++q)
+            while (!mbar_test_wait(smem_u32(&bar[1]), 0)) {
+            }
+          tc_fence_after();
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              tc_mma_bf16(tmem + 32, make_sdesc_sw128(sa + kk * 32, 16, 1024), make_sdesc_sw128(sb + kk * 32, 16, 1024), idesc, 1);
+          for (int q = 0; q < 4; ++q) tc_commit(&bar[4 + q]);
+        }
+      }
+      for (int i = 0; i < (variant >= 4 ? 0 : 16); ++i) {
+        if (variant == 1) {
+          while (!mbar_test_wait(smem_u32(&bar[1]), 0)) {
+          }
+        }
+        if (variant >= 2) {  // smem flag read (ld.acquire.cta) instead of an mbarrier probe
+          uint32_t v;
+          do {
+            asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(slot + 2)) : "memory");
+          } while (v == 0);
+        }
+        if (variant >= 2) tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc_mma_bf16(tmem + 32, make_sdesc_sw128(sa + kk * 32, 16, 1024), make_sdesc_sw128(sb + kk * 32, 16, 1024), idesc, 1);
+        if (variant >= 3) tc_commit(&bar[4 + (i & 3)]);
+      }
+      tc_commit(&bar[10 + variant]);
+      mbar_wait(&bar[10 + variant], 0);
+      long long t1 = clock64();
+      dss[16 * 128 + 9 + variant] = (float)(t1 - t0);
+    }
+  }
+  __syncthreads();
   mbar_wait(&bar[1], 0);
   tc_fence_after();
   float v[16];
@@ -152,7 +231,7 @@ int main() {
   float *dss, *dts;
   cudaMalloc(&dA, A.size() * 2);
   cudaMalloc(&dB, B.size() * 2);
-  cudaMalloc(&dss, 16 * 128 * 4 + 64);
+  cudaMalloc(&dss, 16 * 128 * 4 + 128);
   cudaMalloc(&dts, 16 * 128 * 4);
   cudaMemcpy(dA, A.data(), A.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, B.data(), B.size() * 2, cudaMemcpyHostToDevice);
@@ -177,8 +256,12 @@ int main() {
     }
   printf("max |ref| %.4f  max err SS %.3e  TS %.3e  (SS==TS bitwise: %d)\n", mx, ess, ets,
          (int)(memcmp(hss.data(), hts.data(), hss.size() * 4) == 0));
-  float tm[5];
-  cudaMemcpy(tm, dss + 16 * 128, 20, cudaMemcpyDeviceToHost);
+  float tm[15];
+  cudaMemcpy(tm, dss + 16 * 128, 60, cudaMemcpyDeviceToHost);
+  printf("batched per 4 tiles: 4 waits %.0f, 1 wait %.0f clk\n", tm[13], tm[14]);
+  printf("16 tiles x 4 MMAs: plain %.0f, +mbar test_wait %.0f, smem flag + fence %.0f, + commit %.0f clk\n", tm[9], tm[10], tm[11], tm[12]);
+  printf("2 warps x 32 MMAs concurrently: %.0f / %.0f clk\n", tm[7], tm[8]);
+  printf("64 SS MMAs with a commit after every 4: %.0f clk; with a commit after every 16: %.0f clk\n", tm[5], tm[6]);
   printf("64 SS MMAs over 4 accumulators: %.0f clk; 64 SS MMAs N=64 (B rows beyond 16 = garbage smem): %.0f clk\n", tm[3], tm[4]);
   printf("64 MMAs SS: %.0f clk (%.1f clk/MMA), TS: %.0f clk (%.1f clk/MMA); 64 cp 128x256b: %.0f clk\n", tm[0], tm[0] / 64,
          tm[1], tm[1] / 64, tm[2]);
