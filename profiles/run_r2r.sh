@@ -1,0 +1,4 @@
+timeout 200 python -m pytest tests/test_gpu_stream.py -x -q --timeout 60 2>&1 | tail -2
+timeout 60 python profiles/st_time.py 0 1
+timeout 60 python profiles/step_breakdown.py 2>&1
+timeout 60 python profiles/st_phases.py blocks=4 2>&1 | grep "^p [2-5]" | cut -c1-300
