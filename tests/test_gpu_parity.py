@@ -125,3 +125,15 @@ def test_two_steps_match_oracle():
     r2 = oracle_step(layers, r1["params"], x, t, lr=0.1, m=4, seed=9, step=1)
     errs, bad = compare(g[1], r2, r1["params"], 1e-4, 0.1, gpu_base=g[0]["params"])
     assert not bad, bad
+
+
+def test_c4_full_width_parity():
+    # BASELINE config 4 at full size (U-MLP d = 2048, batch 256, m = 32, 8 partitions with the a1
+    # balance [2, 3, ..., 3]: 4 long skip routes, 8-row micro-batches), all partitions on cuda:0 --
+    # the multi-GPU code path with same-device copies
+    cfg = C.C4()
+    gpu, ref, errs, P = _check(cfg.layers, cfg.batch, cfg.m, cfg.n, cfg.checkpoint, cfg.dtype, cfg.lr, cfg.balance)
+    from oracle.schedule import SKIP_F, route_partitions, records
+    want = records(cfg.m, cfg.n, cfg.checkpoint, route_partitions(cfg.layers, cfg.balance))
+    assert np.array_equal(gpu["log"], want)
+    assert int((gpu["log"][:, 2] == SKIP_F).sum()) == 4 * cfg.m
