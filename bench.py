@@ -165,6 +165,8 @@ def run_tgp(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {ws}")
     if ws > 1:
         dist.init_process_group("gloo")
+    # one GPU per rank; on a box with fewer GPUs than ranks (code-path tests only) ranks share devices
+    lrank = lrank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(lrank)
     dev = torch.device("cuda", lrank)
     layers = C.resmlp_stack(BLOCKS, WIDTH)
@@ -249,7 +251,9 @@ def run_tgp(args):
     traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
     if stream:
         try:
+            # captured on the 32-block (n = 1) F task; per block the traffic is the same
             traffic = json.load(open(os.path.join(ROOT, "profiles", "stream_traffic.json")))["dram_bytes_per_launch"]
+            traffic *= (BLOCKS // n) / BLOCKS
         except Exception:
             traffic = None
     cpu = None
