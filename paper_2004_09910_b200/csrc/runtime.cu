@@ -345,7 +345,7 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
     }
     t.dbg = s.st_dbg;
   }
-  c->kernels += 2;  // counter reset + task kernel
+  c->kernels += 1;  // the task kernel (it resets its dependency counters itself)
   return task_stream_launch(s.comp, t, s.st_clusters);
 }
 

@@ -759,6 +759,20 @@ __global__ void __launch_bounds__(224, 1) task_stream_kernel(const __grid_consta
   __syncthreads();
   cluster_sync();
   if (warp == 1) tmem_dealloc(tmem, 64);
+  // the last CTA to finish resets every dependency counter for the next task (no other CTA polls
+  // any more once all have arrived here; the kernel boundary publishes the zeros)
+  const int ncnt = (3 * t.L + 3) * 5;
+  unsigned* done = t.cnt + (size_t)ncnt * CNT_STRIDE;
+  __shared__ int last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    for (int k = threadIdx.x; k < ncnt; k += blockDim.x) t.cnt[(size_t)k * CNT_STRIDE] = 0u;
+    if (threadIdx.x == 0) *done = 0u;
+  }
 }
 
 // c[h] = sum_k gamma[k] W1[h][k], e[h] = sum_k beta[k] W1[h][k] + b1[h]: one warp per row, lanes
@@ -838,7 +852,7 @@ int task_stream_fold(cudaStream_t st, const SLayer* layers, int L, int d, int H)
 
 // ---------------------------------------------------------------------------------------- host
 int task_stream_smem() { return ST_SMEM; }
-int task_stream_counter_bytes(int L) { return (3 * L + 3) * 5 * CNT_STRIDE * 4; }
+int task_stream_counter_bytes(int L) { return ((3 * L + 3) * 5 + 1) * CNT_STRIDE * 4; }
 
 static bool stream_attr() {
   static int done = 0;
@@ -886,11 +900,7 @@ int task_stream_max_clusters(int dev) {
 
 int task_stream_launch(cudaStream_t st, const STask& t, int clusters) {
   if (!stream_attr()) return -3;
-  cudaError_t e = cudaMemsetAsync(t.cnt, 0, (size_t)task_stream_counter_bytes(t.L), st);
-  if (e != cudaSuccess) {
-    set_error("task_stream counter reset: %s", cudaGetErrorString(e));
-    return -3;
-  }
+  cudaError_t e;
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute at[1];
   stream_cfg(cfg, at, clusters, st);

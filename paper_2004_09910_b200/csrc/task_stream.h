@@ -60,7 +60,8 @@ struct STask {
   float* gbuf0;          // backward: inter-block gradient ping-pong [16][d]
   float* gbuf1;
   float* stats;          // [L + 1][d / 32][16][2] LN row statistics per 32-feature chunk
-  unsigned* cnt;         // dependency counters, one per 128-byte line: [(3L + 3) * 5]
+  unsigned* cnt;         // dependency counters, one per 128-byte line: [(3L + 3) * 5 + 1 (done)], zero
+                         // before the launch; the last CTA of the task zeroes them again
   uint64_t seed;
   const uint32_t* step;  // device optimizer step (dropout counter word 3)
   // diagnostics only (nullptr / 0 on the product path): per CTA and phase, %globaltimer stamps

@@ -39,7 +39,7 @@ def test_stream_kernel_is_used():
     assert not P.stream_enabled(0)
     P.close()
     on, off = _kernels_per_step(layers, 64, 4, 1), _kernels_per_step(layers, 64, 4, 0)
-    # F, F', B are one counter reset + one kernel each with the stream kernel
+    # F, F', B are one kernel each with the stream kernel
     assert on < off, (on, off)
 
 
