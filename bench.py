@@ -44,42 +44,62 @@ def _peaks():
 
 
 class ClockSampler:
-    """Samples nvidia-smi clocks / throttle reasons during the timed region."""
+    """Samples nvidia-smi clocks / throttle reasons during the timed region (the recipe's clocks line).
+    Every line is stamped with its host arrival time; only samples inside [begin(), end()] (+ one
+    sampling period of lag) are reported."""
 
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown"]
+    PERIOD_MS = 100
 
     def __init__(self, dev):
         self.dev = dev
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
     def start(self):
+        """Start sampling and wait (<= 3 s) for the first sample, so the timed region is covered."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
-                text=True)
+                 "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 3.0
+            while not self.lines and time.time() < deadline:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(self.PERIOD_MS / 1000.0)  # the sample covering the end of the window
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        lag = self.PERIOD_MS / 1000.0
+        t0 = self.t0 if self.t0 is not None else 0.0
+        t1 = (self.t1 if self.t1 is not None else time.time()) + lag
         sm, mx, reasons = [], [], set()
         names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
+            if not (t0 <= ts <= t1):
+                continue
             p = [q.strip() for q in ln.split(",")]
             if len(p) < 6:
                 continue
@@ -92,7 +112,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "period_ms": self.PERIOD_MS}
 
 
 def _dist():
@@ -209,15 +229,19 @@ def run_tgp(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(k, e2e):
+    def timed(k, e2e, clk=None):
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         k0 = P.kernel_count()
+        if clk:
+            clk.begin()
         a.record()
         losses = [step(e2e) for _ in range(k)]
         b.record()
         b.synchronize()
+        if clk:
+            clk.end()
         ms = a.elapsed_time(b)
         nk = P.kernel_count() - k0
         barrier()
@@ -230,7 +254,7 @@ def run_tgp(args):
         step()
     clk = ClockSampler(lrank)
     clk.start()
-    ms, nk, losses = timed(args.steps, False)
+    ms, nk, losses = timed(args.steps, False, clk)
     clocks = clk.stop()
     e2e_ms, _, _ = timed(args.steps, True)
 
