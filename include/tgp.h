@@ -201,6 +201,12 @@ const char* tgp_last_error(void);
 tgp_status tgp_bench_dominant_gemm(tgp_ctx* ctx, int32_t part, int32_t B, int32_t reps, double* ms, double* bytes,
                                    int64_t* launches);
 
+/* Profile-based balancing input: per-layer device time in ms of a
+ * forward + backward of one micro-batch (B / chunks rows) of local partition `part`, median of
+ * `reps`, measured with CUDA events between the layers on the per-layer kernel path.
+ * ms_per_layer: host array of the partition's layer count.  Feed it to tgp_balance. */
+tgp_status tgp_profile_layers(tgp_ctx* ctx, int32_t part, int32_t B, int32_t reps, double* ms_per_layer);
+
 /* *on = 1 iff local partition `part` runs its F / F' / B tasks as the persistent weight-streaming
  * task kernel (eligible shape and option "stream" on); then tgp_bench_dominant_gemm times that
  * kernel (F_{1,j} launches: *bytes = its algorithmic bytes -- weights plus activations read and

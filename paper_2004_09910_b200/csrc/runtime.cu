@@ -450,6 +450,7 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         break;
       }
     }
+    if (s.prof_ev) TGP_CUDA_TRY(cudaEventRecord(s.prof_ev[l - s.l0], s.comp));  // tgp_profile_layers
     x = y;
   }
   return 0;
@@ -571,6 +572,7 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         break;
       }
     }
+    if (s.prof_ev) TGP_CUDA_TRY(cudaEventRecord(s.prof_ev[(s.l1 - s.l0) + (s.l1 - 1 - l)], s.comp));
     g = dx;
   }
   return 0;

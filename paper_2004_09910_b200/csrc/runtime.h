@@ -104,6 +104,7 @@ struct Stage {
   float* st_c2part = nullptr; // [L][d/256][H] partial column sums of W2
   bool fold_dirty = true;     // weights / LN parameters changed since st_fold was computed
   unsigned long long* st_dbg = nullptr;  // diagnostics (TGP_ST_DEBUG): [grid][2L][ST_DBG_SLOTS]
+  cudaEvent_t* prof_ev = nullptr;  // tgp_profile_layers: per-layer boundary events (forward, then backward)
   void* red_items = nullptr;  // device RedItem[n_red]: column-partial -> gradient reductions of W_j
   int n_red = 0, red_maxd = 0;
   std::vector<TaskGraph> gF, gB;

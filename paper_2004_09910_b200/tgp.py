@@ -68,6 +68,7 @@ _SIGS = {
                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)],
     "tgp_debug_stream_read": [_P, _I32, _P, _I64, ctypes.POINTER(_I64)],
     "tgp_stream_enabled": [_P, _I32, ctypes.POINTER(_I32)],
+    "tgp_profile_layers": [_P, _I32, _I32, _I32, ctypes.POINTER(ctypes.c_double)],
     "tgp_test_gemm_bf16": [_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P],
 }
 
@@ -281,6 +282,13 @@ class Pipeline:
                                              ctypes.byref(n)), "tgp_bench_dominant_gemm")
         return ms.value, by.value, n.value
 
+    def profile_layers(self, part, B, reps=5):
+        """Per-layer forward + backward device time (ms) of local partition `part` (tgp_profile_layers)."""
+        n = len({self.param_info(i)[0] for i in range(self.n_params) if self.param_info(i)[1] == part})
+        out = (ctypes.c_double * max(1, n))()
+        _check(lib().tgp_profile_layers(self.h, part, B, reps, out), "tgp_profile_layers")
+        return [out[k] for k in range(n)]
+
     def stream_enabled(self, part):
         on = _I32()
         _check(lib().tgp_stream_enabled(self.h, part, ctypes.byref(on)), "tgp_stream_enabled")
@@ -288,3 +296,18 @@ class Pipeline:
 
     def set_option(self, name, value):
         _check(lib().tgp_set_option(self.h, name.encode(), int(value)), "tgp_set_option")
+
+
+def balance_by_time(layers, n_parts, *, batch, chunks, device=0, dtype="bf16", reps=5, seed=0):
+    """Profile-based partition ("resource consumption is computed by profiling"):
+    time every layer's forward + backward on one device (tgp_profile_layers, one micro-batch of
+    batch / chunks rows), then the min-max contiguous partition of those costs (tgp_balance).
+    Returns (balance, costs_ms)."""
+    P = Pipeline(layers, chunks=chunks, devices=[device], balance=[len(layers)], checkpoint="never",
+                 max_batch=batch, dtype=dtype, seed=seed)
+    try:
+        P.init_params(seed)
+        costs = P.profile_layers(0, batch, reps)
+    finally:
+        P.close()
+    return balance(costs, n_parts), costs

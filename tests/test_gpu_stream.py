@@ -159,3 +159,20 @@ def test_full_c2_deterministic_and_modes_bitwise():
         assert got[0] == ref[0], (mode, got[0], ref[0])
         for a, b in zip(got[1], ref[1]):
             assert np.array_equal(a, b), mode
+
+
+def test_profile_based_balance():
+    # PAPER.md P:124 (balance by profiling): per-layer forward + backward device times
+    # of the U-MLP (RESMLP blocks, 2d -> d merges, a d -> d head) are positive, the merges cost more
+    # than a head Linear, and the min-max partition of the profiled costs is a valid balance
+    from paper_2004_09910_b200 import balance_by_time
+
+    layers = C.umlp(d=512, levels=2, blocks_per_level=1, mid_blocks=1)
+    bal, costs = balance_by_time(layers, 3, batch=64, chunks=4, reps=5)
+    assert len(costs) == len(layers) and all(c > 0 for c in costs)
+    kinds = [l["kind"] for l in layers]
+    assert sum(bal) == len(layers) and len(bal) == 3 and min(bal) >= 1
+    merge = [c for c, k in zip(costs, kinds) if k == "merge"]
+    assert min(merge) > 0.5 * costs[-1]
+    uni, ucosts = balance_by_time(C.resmlp_stack(8, 512), 4, batch=64, chunks=4, reps=5)
+    assert uni == [2, 2, 2, 2], (uni, ucosts)
