@@ -192,6 +192,7 @@ def run_tgp(args):
     layers = C.resmlp_stack(BLOCKS, WIDTH)
     devices = [-1] * n
     devices[rank] = lrank
+    free0 = torch.cuda.mem_get_info(dev)[0]
     P = Pipeline(layers, chunks=args.chunks, devices=devices, balance=[BLOCKS // n] * n, checkpoint=args.checkpoint,
                  max_batch=BATCH, dtype="bf16", seed=1234)
     if ws > 1:
@@ -201,6 +202,8 @@ def run_tgp(args):
         k, v = kv.split("=")
         P.set_option(k, int(v))
     P.init_params(seed=1234)
+    free1 = torch.cuda.mem_get_info(dev)[0]
+    mem = P.memory(rank)
     first, last = rank == 0, rank == n - 1
     g = torch.Generator(device="cpu").manual_seed(1234)
     x_h = torch.randn(BATCH, WIDTH, generator=g).pin_memory()
@@ -254,7 +257,9 @@ def run_tgp(args):
         step()
     clk = ClockSampler(lrank)
     clk.start()
+    free_t0 = torch.cuda.mem_get_info(dev)[0]
     ms, nk, losses = timed(args.steps, False, clk)
+    free_t1 = torch.cuda.mem_get_info(dev)[0]
     clocks = clk.stop()
     e2e_ms, _, _ = timed(args.steps, True)
 
@@ -299,6 +304,11 @@ def run_tgp(args):
                          "algorithmic_bytes_per_launch": gemm_bytes, "avg_launch_us": gemm_ms * 1e3,
                          "launches_timed": gemm_n, "peak_source": peak_src},
             "clocks": clocks,
+            "memory": {"plan_used_gb": mem["used"] / 1e9, "plan_reserved_gb": mem["reserved"] / 1e9,
+                       "params_gb": mem["params"] / 1e9, "device_delta_gb": (free0 - free1) / 1e9,
+                       "step_alloc_gb": (free_t0 - free_t1) / 1e9, "note": "per partition; all device memory is allocated in "
+                       "tgp_create (device_delta = cudaMemGetInfo before/after create incl. CUDA context "
+                       "growth), nothing on the step path"},
             "loss_first_last": [losses[0], losses[-1]] if losses and losses[0] is not None else None,
         }
         if cpu:

@@ -201,6 +201,12 @@ const char* tgp_last_error(void);
 tgp_status tgp_bench_dominant_gemm(tgp_ctx* ctx, int32_t part, int32_t B, int32_t reps, double* ms, double* bytes,
                                    int64_t* launches);
 
+/* Static memory plan of local partition `part`: *used = bytes the plan uses (parameters, gradients,
+ * operand stash, activation slots, receive arena, workspaces), *reserved = bytes allocated from the
+ * device for it, *params = fp32 master + fp32 gradient (+ bf16 shadow) bytes.  Any pointer may be
+ * NULL.  All of it is allocated in tgp_create; nothing on the step path. */
+tgp_status tgp_memory(tgp_ctx* ctx, int32_t part, int64_t* used, int64_t* reserved, int64_t* params);
+
 /* Profile-based balancing input: per-layer device time in ms of a
  * forward + backward of one micro-batch (B / chunks rows) of local partition `part`, median of
  * `reps`, measured with CUDA events between the layers on the per-layer kernel path.

@@ -63,12 +63,14 @@ void* Pool::get(size_t bytes) {
     if (cudaMalloc(&p, cs) != cudaSuccess) return nullptr;
     if (cudaMemset(p, 0, cs) != cudaSuccess) return nullptr;
     chunks.push_back(p);
+    reserved += cs;
     cur = (char*)p;
     left = cs;
   }
   void* r = cur;
   cur += bytes;
   left -= bytes;
+  used += bytes;
   return r;
 }
 void Pool::release() {

@@ -19,6 +19,7 @@ struct Pool {
   std::vector<void*> chunks;
   char* cur = nullptr;
   size_t left = 0;
+  size_t used = 0, reserved = 0;  // bytes handed out / bytes cudaMalloc'ed (memory accounting)
   void* get(size_t bytes);
   void release();
 };
@@ -73,6 +74,7 @@ struct Stage {
   std::vector<cudaEvent_t> tr_ev;  // timeline events (pairs)
   Pool pool;
   void* arena = nullptr;
+  size_t extra_bytes = 0;  // device allocations outside the pool (arena, descriptors, tables)
   ArenaView self;
   float* out = nullptr;     // [max_batch][d_out] stage output (message source)
   float* dx_out = nullptr;  // [max_batch][d_in] input gradient (message source)

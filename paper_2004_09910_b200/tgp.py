@@ -69,6 +69,7 @@ _SIGS = {
     "tgp_debug_stream_read": [_P, _I32, _P, _I64, ctypes.POINTER(_I64)],
     "tgp_stream_enabled": [_P, _I32, ctypes.POINTER(_I32)],
     "tgp_profile_layers": [_P, _I32, _I32, _I32, ctypes.POINTER(ctypes.c_double)],
+    "tgp_memory": [_P, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
     "tgp_test_gemm_bf16": [_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P],
 }
 
@@ -288,6 +289,12 @@ class Pipeline:
         out = (ctypes.c_double * max(1, n))()
         _check(lib().tgp_profile_layers(self.h, part, B, reps, out), "tgp_profile_layers")
         return [out[k] for k in range(n)]
+
+    def memory(self, part):
+        """Static memory plan of local partition `part`: dict(used, reserved, params) in bytes."""
+        u, r, p = _I64(), _I64(), _I64()
+        _check(lib().tgp_memory(self.h, part, ctypes.byref(u), ctypes.byref(r), ctypes.byref(p)), "tgp_memory")
+        return {"used": u.value, "reserved": r.value, "params": p.value}
 
     def stream_enabled(self, part):
         on = _I32()
