@@ -93,6 +93,17 @@ tgp_status tgp_split(int32_t B, int32_t m, int32_t* sizes_out);
 tgp_status tgp_schedule(int32_t m, int32_t n, tgp_checkpoint ckpt, const int32_t* routes, int32_t n_routes,
                         int32_t* rec, int64_t cap, int64_t* n_rec);
 
+/* The same records under the Table 1 ablation toggles that
+ * tgp_set_option's "ablate_portals" / "ablate_order" select: relay != 0 tuple-threads every skip
+ * tensor through each partition between stash and pop (SKIP_F hop j-1 -> j issued with F_{i,j},
+ * SKIP_B hop j+1 -> j with B_{i,j}, for every j the route spans) instead of one portal copy;
+ * order_seed != 0 replaces the mirrored backward clocks by a seeded random topological order of
+ * the backward tasks (each B_{i,j} with its COPY_B / SKIP_B messages and F'_{i,j} before it; the
+ * clock field is then the issue step), emulating an autograd engine without Fork/Join edges.
+ * relay = 0 and order_seed = 0 give exactly tgp_schedule's records. */
+tgp_status tgp_schedule_ablation(int32_t m, int32_t n, tgp_checkpoint ckpt, const int32_t* routes, int32_t n_routes,
+                                 int32_t relay, uint64_t order_seed, int32_t* rec, int64_t cap, int64_t* n_rec);
+
 /* ------------------------------------------------------------------ context */
 
 /* Create a pipeline.  layers[n_layers] as above; balance[n_parts] layers per partition (NULL:
@@ -181,6 +192,15 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *             weight-streaming kernel per task (task_stream.cu; default 1 where eligible)
  *  "dw_persistent" deferred weight gradients through the persistent 128x128-tile dW kernel (default 1)
  *  "stream_poll_ns" back-off of the stream kernel's dependency polling loops, ns (default 32)
+ * Table 1 ablation toggles (results are bitwise those of the default -- only the
+ * issue order and the copy path change).  Need every partition in this process, and not between
+ * forward and backward (TGP_E_UNSUPPORTED / TGP_E_STATE):
+ *  "ablate_order"        value = seed != 0: backward tasks in tgp_schedule_ablation's random
+ *                        topological order instead of the Fork/Join order (0 = off)
+ *  "ablate_copy_streams" 1 = copies on the producer's compute stream, waiting for all work issued
+ *                        on the consumer's compute stream and waited on by it (default-stream copies)
+ *  "ablate_portals"      1 = skip tensors relayed through every partition in between (extra relay
+ *                        slots, allocated here and counted by tgp_memory; 0 frees them)
  * Test-only negative controls (never used on the product path):
  *  "test_poison"        fill the forward receive slabs with NaN before each forward call
  *  "test_skip_wait"     drop the receive waits of partition `value` (-1 = none)
@@ -205,6 +225,10 @@ tgp_status tgp_bench_dominant_gemm(tgp_ctx* ctx, int32_t part, int32_t B, int32_
  * operand stash, activation slots, receive arena, workspaces), *reserved = bytes allocated from the
  * device for it, *params = fp32 master + fp32 gradient (+ bf16 shadow) bytes.  Any pointer may be
  * NULL.  All of it is allocated in tgp_create; nothing on the step path. */
+/* Messages (activation, gradient and skip copies) this process pushed since creation: *bytes
+ * payload bytes, *messages count.  Either pointer may be NULL. */
+tgp_status tgp_copy_stats(tgp_ctx* ctx, int64_t* bytes, int64_t* messages);
+
 tgp_status tgp_memory(tgp_ctx* ctx, int32_t part, int64_t* used, int64_t* reserved, int64_t* params);
 
 /* Profile-based balancing input: per-layer device time in ms of a

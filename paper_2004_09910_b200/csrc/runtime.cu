@@ -702,6 +702,24 @@ static void micro_rows(const tgp_ctx* c, int B, int i, int* r0, int* M) {
   *M = q + (ii < r ? 1 : 0);
 }
 
+// an event of stage s's device (reused every call; the waits bind at enqueue time)
+static cudaEvent_t abl_event(Stage& s) {
+  if (s.abl_next == s.abl_events.size()) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(s.dev);
+    cudaEvent_t e = nullptr;
+    const cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaSetDevice(cur);
+    if (err != cudaSuccess) {
+      set_error("cudaEventCreate failed: %s", cudaGetErrorString(err));
+      return nullptr;
+    }
+    s.abl_events.push_back(e);
+  }
+  return s.abl_events[s.abl_next++];
+}
+
 // partitions that push data into partition j (receive arena writers)
 static std::vector<int> writers_of(const tgp_ctx* c, int j) {
   std::vector<int> w;
@@ -737,6 +755,16 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       const bool skip = rc.kind == K_SKIP_F || rc.kind == K_SKIP_B;
       cudaStream_t st = skip ? s.cskip : s.cact;
       cudaEvent_t ev = (rc.kind == K_COPY_F || rc.kind == K_SKIP_F) ? s.fdone[i - 1] : s.bdone[i - 1];
+      if (c->abl_streams) {
+        // Table 1 "no copy streams" ablation: the copy rides on the producer's compute stream and,
+        // like a default-stream copy (Fig. 5), first waits for all work issued so far on the
+        // consumer's compute stream
+        st = s.comp;
+        cudaEvent_t e = abl_event(*c->local[dst]);
+        if (!e) return TGP_E_CUDA;
+        TGP_CUDA_TRY(cudaEventRecord(e, c->local[dst]->comp));
+        TGP_CUDA_TRY(cudaStreamWaitEvent(st, e, 0));
+      }
       TGP_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
       if (!first_push[src][dst]) {
         // the consumer must have finished the previous call before its receive slots are reused
@@ -751,22 +779,48 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       cudaEvent_t ta = nullptr;
       trace_begin(c, s, st, skip ? 2 : 1, rc.kind, i, &ta);
       uint32_t* ctr = s.counters + (skip ? 1 : 0);
+      int64_t nbytes = 0;
       if (rc.kind == K_COPY_F) {
+        nbytes = (int64_t)M * s.d_out * 4;
         TGP_TRY(push_rows(st, s.out + (size_t)r0 * s.d_out, pv.fwd_in + (size_t)r0 * s.d_out, false,
                           (int64_t)M * s.d_out, ctr, flag_fwd(pv, i), seq));
       } else if (rc.kind == K_COPY_B) {
+        nbytes = (int64_t)M * s.d_in * 4;
         TGP_TRY(push_rows(st, s.dx_out + (size_t)r0 * s.d_in, pv.grad_in + (size_t)r0 * s.d_in, false,
                           (int64_t)M * s.d_in, ctr, flag_grad(c, pv, i), seq));
       } else if (rc.kind == K_SKIP_F) {
+        // portal: stash partition -> pop partition; relay (ablation): hop src -> dst through the
+        // relay slots of the partitions in between
         const Route& R = c->routes[rc.route];
-        const int64_t nb = (int64_t)M * R.width * op_size(c);
-        TGP_TRY(push_bytes(st, opptr(c, s.skip_send[R.id], r0, R.width), opptr(c, pv.skip_in[R.id], r0, R.width), nb, ctr,
+        nbytes = (int64_t)M * R.width * op_size(c);
+        void* from = src == R.src ? s.skip_send[R.id] : s.relay_skip[R.id];
+        void* to = dst == R.dst ? pv.skip_in[R.id] : c->local[dst]->relay_skip[R.id];
+        if (!from || !to) {
+          set_error("skip route %d: no buffer for hop %d -> %d", R.id, src, dst);
+          return TGP_E_STATE;
+        }
+        TGP_TRY(push_bytes(st, opptr(c, from, r0, R.width), opptr(c, to, r0, R.width), nbytes, ctr,
                            flag_skip(c, pv, R.id, i), seq));
       } else {
         const Route& R = c->routes[rc.route];
-        TGP_TRY(push_rows(st, s.dskip_send[R.id] + (size_t)r0 * R.width, pv.dskip_in[R.id] + (size_t)r0 * R.width,
-                          false, (int64_t)M * R.width, ctr, flag_dskip(c, pv, R.id, i), seq));
+        nbytes = (int64_t)M * R.width * 4;
+        float* from = src == R.dst ? s.dskip_send[R.id] : s.relay_dskip[R.id];
+        float* to = dst == R.src ? pv.dskip_in[R.id] : c->local[dst]->relay_dskip[R.id];
+        if (!from || !to) {
+          set_error("skip route %d: no gradient buffer for hop %d -> %d", R.id, src, dst);
+          return TGP_E_STATE;
+        }
+        TGP_TRY(push_rows(st, from + (size_t)r0 * R.width, to + (size_t)r0 * R.width, false, (int64_t)M * R.width, ctr,
+                          flag_dskip(c, pv, R.id, i), seq));
       }
+      if (c->abl_streams) {  // the consumer's later work waits for the copy (default-stream semantics)
+        cudaEvent_t e = abl_event(s);
+        if (!e) return TGP_E_CUDA;
+        TGP_CUDA_TRY(cudaEventRecord(e, st));
+        TGP_CUDA_TRY(cudaStreamWaitEvent(c->local[dst]->comp, e, 0));
+      }
+      c->copy_bytes += nbytes;
+      c->copy_msgs++;
       c->kernels++;
       trace_end(c, s, st, skip ? 2 : 1, rc.kind, i, ta);
       c->issue_log.push_back(rc);
@@ -780,13 +834,16 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       if (!sp) return 0;
       Stage& s = *sp;
       if (rc.kind == K_F && j > 0 && c->skip_wait_part != j) TGP_TRY(wait_flag(c, s.comp, flag_fwd(s.self, i), seq));
+      // relay (ablation): a partition between stash and pop takes the skip tensor as a tuple input
+      // of F and its gradient as a tuple input of B
+      auto relays = [&](const Route& R) { return c->relay && R.src < j && j < R.dst; };
       if (rc.kind == K_F)
         for (const Route& R : c->routes)
-          if (R.dst == j && R.src != j) TGP_TRY(wait_flag(c, s.comp, flag_skip(c, s.self, R.id, i), seq));
+          if ((R.dst == j && R.src != j) || relays(R)) TGP_TRY(wait_flag(c, s.comp, flag_skip(c, s.self, R.id, i), seq));
       if (rc.kind == K_B) {
         if (j < c->n - 1 && c->skip_wait_part != j) TGP_TRY(wait_flag(c, s.comp, flag_grad(c, s.self, i), seq));
         for (const Route& R : c->routes)
-          if (R.src == j && R.dst != j) TGP_TRY(wait_flag(c, s.comp, flag_dskip(c, s.self, R.id, i), seq));
+          if ((R.src == j && R.dst != j) || relays(R)) TGP_TRY(wait_flag(c, s.comp, flag_dskip(c, s.self, R.id, i), seq));
       }
       cudaEvent_t ta = nullptr;
       trace_begin(c, s, s.comp, 0, rc.kind, i, &ta);
@@ -860,6 +917,8 @@ static int finish_call(tgp_ctx* c) {
 
 static int begin_call(tgp_ctx* c) {
   c->seq++;
+  for (Stage* s : c->local)
+    if (s) s->abl_next = 0;
   for (int j = 0; j < c->n; ++j) {
     Stage* sp = c->local[j];
     if (!sp) continue;
@@ -902,30 +961,50 @@ tgp_status tgp_split(int32_t B, int32_t m, int32_t* sizes) {
   return TGP_OK;
 }
 
-tgp_status tgp_schedule(int32_t m, int32_t n, tgp_checkpoint ckpt, const int32_t* routes, int32_t n_routes,
-                        int32_t* rec, int64_t cap, int64_t* n_rec) {
+static tgp_status schedule_impl(const char* who, int32_t m, int32_t n, tgp_checkpoint ckpt, const int32_t* routes,
+                                int32_t n_routes, bool relay, uint64_t order_seed, int32_t* rec, int64_t cap,
+                                int64_t* n_rec) {
   if (m < 1 || n < 1 || (int)ckpt < 0 || (int)ckpt > 2 || n_routes < 0 || (n_routes > 0 && !routes)) {
-    set_error("tgp_schedule: bad arguments");
+    set_error("%s: bad arguments", who);
     return TGP_E_INVALID;
   }
   std::vector<std::pair<int, int>> r;
   for (int q = 0; q < n_routes; ++q) {
     if (routes[2 * q] < 1 || routes[2 * q + 1] < routes[2 * q] || routes[2 * q + 1] > n) {
-      set_error("tgp_schedule: route %d must satisfy 1 <= src <= dst <= n", q);
+      set_error("%s: route %d must satisfy 1 <= src <= dst <= n", who, q);
       return TGP_E_INVALID;
     }
     r.emplace_back(routes[2 * q], routes[2 * q + 1]);
   }
-  auto recs = emit_schedule(m, n, (int)ckpt, r);
+  auto recs = emit_schedule(m, n, (int)ckpt, r, relay);
+  if (order_seed) {
+    std::vector<Rec> f, w;
+    for (const Rec& x : recs) (x.phase == 0 ? f : w).push_back(x);
+    auto b = unordered_backward(m, n, (int)ckpt, r, relay, order_seed);
+    recs = f;
+    for (const Rec& x : b) recs.push_back(x);
+    for (const Rec& x : w)
+      if (x.phase == 2) recs.push_back(x);
+  }
   if (n_rec) *n_rec = (int64_t)recs.size();
   if (rec) {
     if (cap < (int64_t)recs.size()) {
-      set_error("tgp_schedule: cap %lld < %zu records", (long long)cap, recs.size());
+      set_error("%s: cap %lld < %zu records", who, (long long)cap, recs.size());
       return TGP_E_INVALID;
     }
     memcpy(rec, recs.data(), recs.size() * sizeof(Rec));
   }
   return TGP_OK;
+}
+
+tgp_status tgp_schedule(int32_t m, int32_t n, tgp_checkpoint ckpt, const int32_t* routes, int32_t n_routes,
+                        int32_t* rec, int64_t cap, int64_t* n_rec) {
+  return schedule_impl("tgp_schedule", m, n, ckpt, routes, n_routes, false, 0, rec, cap, n_rec);
+}
+
+tgp_status tgp_schedule_ablation(int32_t m, int32_t n, tgp_checkpoint ckpt, const int32_t* routes, int32_t n_routes,
+                                 int32_t relay, uint64_t order_seed, int32_t* rec, int64_t cap, int64_t* n_rec) {
+  return schedule_impl("tgp_schedule_ablation", m, n, ckpt, routes, n_routes, relay != 0, order_seed, rec, cap, n_rec);
 }
 
 }  // extern "C"

@@ -81,6 +81,13 @@ struct Stage {
   std::vector<void*> skip_send;     // route id -> [max_batch][w] op dtype (src side, cross routes)
   std::vector<float*> dskip_send;   // route id -> [max_batch][w] fp32 (dst side, cross routes)
   std::vector<float*> dskip_local;  // route id -> [mb_cap][w] fp32 (src == dst)
+  // Table 1 "no portals" ablation (option "ablate_portals"): tuple-threaded skip tensors held by
+  // the partitions strictly between a route's stash and pop partitions
+  std::vector<void*> relay_skip;    // route id -> [max_batch][w] op dtype (forward relay slot)
+  std::vector<float*> relay_dskip;  // route id -> [max_batch][w] fp32 (backward relay slot)
+  size_t relay_bytes = 0;
+  std::vector<cudaEvent_t> abl_events;  // "ablate_copy_streams": events recorded on this stage's streams
+  size_t abl_next = 0;
   float *master = nullptr, *grad = nullptr;
   __nv_bfloat16* shadow = nullptr;
   int64_t n_elems = 0;
@@ -148,6 +155,11 @@ struct tgp_ctx {
   int st_flags = 0;
   bool dw_persistent = true;  // deferred dW through the persistent gemm_dw kernel (option "dw_persistent")
   unsigned st_sleep_ns = 32;  // stream kernel: back-off between dependency polls (option "stream_poll_ns")  // test only: bit 0 = stream kernel ignores dependencies (timing of the bare weight stream)  // persistent weight-streaming task kernel where eligible (task_stream.cu)
+  // Table 1 ablation toggles: 0 / false = the torchgpipe design
+  uint64_t order_seed = 0;   // "ablate_order": backward tasks in a seeded random topological order
+  bool relay = false;        // "ablate_portals": skip tensors tuple-threaded through every partition
+  bool abl_streams = false;  // "ablate_copy_streams": copies on the compute streams, two-way synchronised
+  int64_t copy_bytes = 0, copy_msgs = 0;  // messages this process pushed since creation
   int splitk = 0, skip_wait_part = -1;
   uint64_t delay_push_ns = 0;
   bool can_flush = false;

@@ -41,6 +41,9 @@ _SIGS = {
     "tgp_split": [_I32, _I32, ctypes.POINTER(_I32)],
     "tgp_schedule": [_I32, _I32, _I32, ctypes.POINTER(_I32), _I32, ctypes.POINTER(_I32), _I64,
                      ctypes.POINTER(_I64)],
+    "tgp_schedule_ablation": [_I32, _I32, _I32, ctypes.POINTER(_I32), _I32, _I32, ctypes.c_uint64,
+                              ctypes.POINTER(_I32), _I64, ctypes.POINTER(_I64)],
+    "tgp_copy_stats": [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
     "tgp_create": [ctypes.POINTER(Layer), _I32, ctypes.POINTER(_I32), _I32, _I32, _I32, ctypes.POINTER(_I32),
                    _I32, _I32, ctypes.c_uint64, ctypes.POINTER(_P)],
     "tgp_destroy": [_P],
@@ -131,14 +134,20 @@ def split(B, m):
     return list(out)
 
 
-def schedule(m, n, checkpoint="except_last", routes=()):
+def schedule(m, n, checkpoint="except_last", routes=(), relay=False, order_seed=0):
+    """tgp_schedule records [n_rec][8]; relay / order_seed select the Table 1 ablation variants
+    (tgp_schedule_ablation)."""
     routes = list(routes)
     r = (_I32 * max(1, 2 * len(routes)))(*[v for pr in routes for v in pr])
     cnt = _I64()
-    _check(lib().tgp_schedule(m, n, CKPT[checkpoint], r, len(routes), None, 0, ctypes.byref(cnt)), "tgp_schedule")
+    if relay or order_seed:
+        call = lambda buf, cap: lib().tgp_schedule_ablation(m, n, CKPT[checkpoint], r, len(routes), int(bool(relay)),
+                                                             order_seed, buf, cap, ctypes.byref(cnt))
+    else:
+        call = lambda buf, cap: lib().tgp_schedule(m, n, CKPT[checkpoint], r, len(routes), buf, cap, ctypes.byref(cnt))
+    _check(call(None, 0), "tgp_schedule")
     buf = (_I32 * (8 * cnt.value))()
-    _check(lib().tgp_schedule(m, n, CKPT[checkpoint], r, len(routes), buf, cnt.value, ctypes.byref(cnt)),
-           "tgp_schedule")
+    _check(call(buf, cnt.value), "tgp_schedule")
     return np.frombuffer(buf, dtype=np.int32).reshape(-1, 8).copy()
 
 
@@ -295,6 +304,12 @@ class Pipeline:
         u, r, p = _I64(), _I64(), _I64()
         _check(lib().tgp_memory(self.h, part, ctypes.byref(u), ctypes.byref(r), ctypes.byref(p)), "tgp_memory")
         return {"used": u.value, "reserved": r.value, "params": p.value}
+
+    def copy_stats(self):
+        """(payload bytes, messages) pushed by this process since creation (tgp_copy_stats)."""
+        b, n = _I64(), _I64()
+        _check(lib().tgp_copy_stats(self.h, ctypes.byref(b), ctypes.byref(n)), "tgp_copy_stats")
+        return b.value, n.value
 
     def stream_enabled(self, part):
         on = _I32()
