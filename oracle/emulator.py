@@ -27,7 +27,7 @@ from .schedule import (B as K_B, COPY_B, COPY_F, F as K_F, RECOMPUTE, SKIP_B, SK
 def emulate(layers, params, x, t, *, balance, m, mode, seed=0, step=0):
     n = len(balance)
     Bsz = x.shape[0]
-    off = split_offsets(Bsz, m)
+    off = M.micro_offsets(layers, Bsz, m)
     P = M.group_params(layers, params)
     starts = [0]
     for c in balance:
@@ -119,7 +119,7 @@ def emulate(layers, params, x, t, *, balance, m, mode, seed=0, step=0):
             if j == n and dy_full is None:
                 assert all((ii, n) in out for ii in range(1, m + 1)), "loss before all outputs"
                 y_all = np.concatenate([out[(ii, n)] for ii in range(1, m + 1)], axis=0)
-                loss, dy_full = M.mse(y_all, t)
+                loss, dy_full = M.loss_fn(layers, y_all, t)
             if i < m:
                 assert (i + 1, j) in done_B, "B order violated"
             tag, caches = saved[(i, j)]

@@ -22,6 +22,21 @@ Layer formulas (O2) and textbook VJPs (O4):
   ReLU'   [z > 0]  (derivative at 0 taken as 0)
   loss    L = sum (y-t)^2 / (B d_out);  dy = 2 (y-t) / (B d_out)   (O3, reading Z10)
   SGD     theta' = theta - lr g   ("trained by plain SGD")
+
+GPT-2-shaped layers (C5, BASELINE.json configs[4]; reading Z13 -- the paper names GPT-2 1.5B as
+a GPipe workload, but gives no formulas, so these are the textbook definitions).  Rows are
+TOKENS; a sample is a sequence of `seq` tokens and micro-batches hold whole sequences.
+  embed   y = wte[id] + wpe[pos] [* keep/(1-p)]   (id = token id carried in x[:, 0], pos = row % seq)
+  block   h1 = LN1(x); qkv = h1 Wqkv^T + bqkv; per sequence and head (dh = d / n_heads):
+          S = q k^T / sqrt(dh), causal (key <= query), P = softmax_row(S), Pd = P * keep/(1-p),
+          ctx = Pd v; x1 = x + drop(ctx Wo^T + bo); h2 = LN2(x1); z = h2 W1^T + b1;
+          y = x1 + drop(GELU(z) W2^T + b2)
+          VJP of softmax: dS = P * (dP - rowsum(P * dP)), dP = dPd * keep/(1-p)
+  lmhead  y = LN(x) W^T   (logits, no bias)
+  CE      L = mean_t (logsumexp(y_t) - y_t[target_t]);  dy = (softmax(y) - onehot(target)) / T
+Dropout sites (Philox counter word 2): embed / resmlp / linear: layer index; block: layer index
++ 1<<16 (attention probabilities, indexed in the [n_seq, n_heads, seq, seq] tensor), + 2<<16
+(attention residual branch), + 3<<16 (MLP residual branch).
 """
 import numpy as np
 from scipy.special import erf
@@ -56,7 +71,99 @@ def act_df(name, z):
 
 
 def n_params(L):
-    return {"linear": 2, "merge": 2, "resmlp": 6, "batchnorm": 2}[L["kind"]]
+    return {"linear": 2, "merge": 2, "resmlp": 6, "batchnorm": 2, "embed": 2, "transformer": 12,
+            "lmhead": 3}[L["kind"]]
+
+
+def row_unit(layers):
+    """Rows per sample: `seq` tokens for the GPT-2-shaped layers, else 1."""
+    return max([int(L.get("seq", 0)) for L in layers] + [1])
+
+
+def micro_offsets(layers, rows, m):
+    """Row offsets of the m micro-batches: split the samples (reading Z7), then scale to rows."""
+    u = row_unit(layers)
+    assert rows % u == 0, "rows must be whole samples"
+    return [o * u for o in split_offsets(rows // u, m)]
+
+
+SITE_ATTN, SITE_RES1, SITE_RES2 = 1 << 16, 2 << 16, 3 << 16
+
+
+def _ln_fwd(x, gamma, beta):
+    mu = x.mean(axis=1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=1, keepdims=True)
+    r = 1.0 / np.sqrt(var + LN_EPS)
+    nrm = (x - mu) * r
+    return gamma * nrm + beta, (r, nrm)
+
+
+def _ln_bwd(dh, gamma, c):
+    r, nrm = c
+    dn = dh * gamma
+    dx = r * (dn - dn.mean(axis=1, keepdims=True) - nrm * (dn * nrm).mean(axis=1, keepdims=True))
+    return dx, (dh * nrm).sum(axis=0), dh.sum(axis=0)
+
+
+def _attn_fwd(qkv, nh, seq, pdrop, seed, step, site, row0):
+    """Causal multi-head attention on whole sequences; row0 = global token row of qkv[0]."""
+    T, d3 = qkv.shape
+    d = d3 // 3
+    dh = d // nh
+    ctx = np.zeros((T, d))
+    cache = {}
+    for s in range(T // seq):
+        sg = (row0 // seq) + s                       # global sequence index
+        rs = slice(s * seq, (s + 1) * seq)
+        for h in range(nh):
+            q = qkv[rs, h * dh:(h + 1) * dh]
+            k = qkv[rs, d + h * dh:d + (h + 1) * dh]
+            v = qkv[rs, 2 * d + h * dh:2 * d + (h + 1) * dh]
+            S = q @ k.T / np.sqrt(dh)
+            S = np.where(np.tril(np.ones((seq, seq), bool)), S, -np.inf)
+            P = np.exp(S - S.max(axis=1, keepdims=True))
+            P = P / P.sum(axis=1, keepdims=True)
+            keep = None
+            Pd = P
+            if pdrop > 0:
+                keep = dropout_keep(seed, step, site, (sg * nh + h) * seq, seq, seq, pdrop)
+                Pd = P * keep / (1.0 - pdrop)
+            ctx[rs, h * dh:(h + 1) * dh] = Pd @ v
+            cache[(s, h)] = (P, keep)
+    return ctx, cache
+
+
+def _attn_bwd(qkv, dctx, nh, seq, pdrop, cache):
+    T, d3 = qkv.shape
+    d = d3 // 3
+    dh = d // nh
+    dqkv = np.zeros_like(qkv)
+    for s in range(T // seq):
+        rs = slice(s * seq, (s + 1) * seq)
+        for h in range(nh):
+            cq, ck, cv = (slice(o + h * dh, o + (h + 1) * dh) for o in (0, d, 2 * d))
+            q, k, v = qkv[rs, cq], qkv[rs, ck], qkv[rs, cv]
+            P, keep = cache[(s, h)]
+            Pd = P if keep is None else P * keep / (1.0 - pdrop)
+            do = dctx[rs, h * dh:(h + 1) * dh]
+            dPd = do @ v.T
+            dqkv[rs, cv] = Pd.T @ do
+            dP = dPd if keep is None else dPd * keep / (1.0 - pdrop)
+            dS = P * (dP - (P * dP).sum(axis=1, keepdims=True))
+            dqkv[rs, cq] = dS @ k / np.sqrt(dh)
+            dqkv[rs, ck] = dS.T @ q / np.sqrt(dh)
+    return dqkv
+
+
+def _drop(a, pdrop, seed, step, site, row0):
+    if pdrop <= 0:
+        return a, None
+    keep = dropout_keep(seed, step, site, row0, a.shape[0], a.shape[1], pdrop)
+    return a * keep / (1.0 - pdrop), keep
+
+
+def _undrop(da, keep, pdrop):
+    return da if keep is None else da * keep / (1.0 - pdrop)
 
 
 def group_params(layers, params):
@@ -102,6 +209,28 @@ def layer_fwd(L, p, x, s, *, site, seed, step, row0, groups):
             g = g * keep / (1.0 - pdrop)
         y = x + g @ W2.T + b2
         return y, (x, r, nrm, h, a, g, keep)
+    if k == "embed":
+        wte, wpe = p
+        ids = np.rint(x[:, 0]).astype(np.int64)
+        pos = (row0 + np.arange(rows)) % L["seq"]
+        y, keep = _drop(wte[ids] + wpe[pos], pdrop, seed, step, site, row0)
+        return y, (ids, pos, keep)
+    if k == "transformer":
+        g1, be1, Wqkv, bqkv, Wo, bo, g2, be2, W1, b1, W2, b2 = p
+        h1, c1 = _ln_fwd(x, g1, be1)
+        qkv = h1 @ Wqkv.T + bqkv
+        ctx, ca = _attn_fwd(qkv, L["n_heads"], L["seq"], pdrop, seed, step, site + SITE_ATTN, row0)
+        ao, k1 = _drop(ctx @ Wo.T + bo, pdrop, seed, step, site + SITE_RES1, row0)
+        x1 = x + ao
+        h2, c2 = _ln_fwd(x1, g2, be2)
+        z = h2 @ W1.T + b1
+        g = act_f("gelu", z)
+        mo, k2 = _drop(g @ W2.T + b2, pdrop, seed, step, site + SITE_RES2, row0)
+        return x1 + mo, (h1, c1, qkv, ctx, ca, k1, x1, h2, c2, z, g, k2)
+    if k == "lmhead":
+        gamma, beta, W = p
+        h, c = _ln_fwd(x, gamma, beta)
+        return h @ W.T, (h, c)
     if k == "batchnorm":
         gamma, beta = p
         y = np.empty_like(x)
@@ -153,6 +282,35 @@ def layer_bwd(L, p, cache, dy, *, groups):
         dn = dh * gamma
         dx_ln = r * (dn - dn.mean(axis=1, keepdims=True) - nrm * (dn * nrm).mean(axis=1, keepdims=True))
         return dy + dx_ln, None, [dgamma, dbeta, dW1, db1, dW2, db2]
+    if k == "embed":
+        wte, wpe = p
+        ids, pos, keep = cache
+        de = _undrop(dy, keep, pdrop)
+        dwte = np.zeros_like(wte)
+        np.add.at(dwte, ids, de)
+        dwpe = np.zeros_like(wpe)
+        np.add.at(dwpe, pos, de)
+        return np.zeros((dy.shape[0], 1)), None, [dwte, dwpe]
+    if k == "transformer":
+        g1, be1, Wqkv, bqkv, Wo, bo, g2, be2, W1, b1, W2, b2 = p
+        h1, c1, qkv, ctx, ca, k1, x1, h2, c2, z, g, k2 = cache
+        dm = _undrop(dy, k2, pdrop)                       # MLP branch
+        dW2, db2 = dm.T @ g, dm.sum(axis=0)
+        dz = (dm @ W2) * act_df("gelu", z)
+        dW1, db1 = dz.T @ h2, dz.sum(axis=0)
+        dx1_ln, dg2, dbe2 = _ln_bwd(dz @ W1, g2, c2)
+        dx1 = dy + dx1_ln
+        da = _undrop(dx1, k1, pdrop)                      # attention branch
+        dWo, dbo = da.T @ ctx, da.sum(axis=0)
+        dqkv = _attn_bwd(qkv, da @ Wo, L["n_heads"], L["seq"], pdrop, ca)
+        dWqkv, dbqkv = dqkv.T @ h1, dqkv.sum(axis=0)
+        dx_ln, dg1, dbe1 = _ln_bwd(dqkv @ Wqkv, g1, c1)
+        return dx1 + dx_ln, None, [dg1, dbe1, dWqkv, dbqkv, dWo, dbo, dg2, dbe2, dW1, db1, dW2, db2]
+    if k == "lmhead":
+        gamma, beta, W = p
+        h, c = cache
+        dx, dg, db = _ln_bwd(dy @ W, gamma, c)
+        return dx, None, [dg, db, dy.T @ h]
     if k == "batchnorm":
         gamma, beta = p
         dx = np.empty_like(dy)
@@ -173,7 +331,7 @@ def forward(layers, params, x, *, m=1, seed=0, step=0, row0=0):
     """Forward over the full mini-batch (rows row0.. of the global batch).  Returns (y, caches)."""
     P = group_params(layers, params)
     h = np.asarray(x, dtype=np.float64)
-    off = split_offsets(h.shape[0], m)
+    off = micro_offsets(layers, h.shape[0], m)
     groups = [(off[i], off[i + 1]) for i in range(m)]
     skips, caches = {}, []
     for li, L in enumerate(layers):
@@ -210,6 +368,25 @@ def mse(y, t):
     return float((diff ** 2).sum() / (B * d)), 2.0 * diff / (B * d)
 
 
+def cross_entropy(y, t):
+    """Mean token cross-entropy on logits y [T, V] with integer targets t [T] (O3, C5)."""
+    T = y.shape[0]
+    t = np.asarray(t).reshape(-1).astype(np.int64)
+    mx = y.max(axis=1, keepdims=True)
+    e = np.exp(y - mx)
+    se = e.sum(axis=1, keepdims=True)
+    lse = (mx + np.log(se))[:, 0]
+    loss = float((lse - y[np.arange(T), t]).sum() / T)
+    dy = e / se
+    dy[np.arange(T), t] -= 1.0
+    return loss, dy / T
+
+
+def loss_fn(layers, y, t):
+    """CE for models ending in an LM head, else MSE."""
+    return cross_entropy(y, t) if layers[-1]["kind"] == "lmhead" else mse(y, t)
+
+
 def bn_running(layers, caches, running=None):
     """Commit BN running statistics once per step from the full mini-batch (O9 / reading Z18):
     rm <- (1-mom) rm + mom mean_B;  rv <- (1-mom) rv + mom var_B * B/(B-1),
@@ -234,7 +411,7 @@ def bn_running(layers, caches, running=None):
 def train_step(layers, params, x, t, *, lr, m=1, seed=0, step=0, want_dx=True):
     """One unpipelined fp64 training step on the whole mini-batch."""
     y, caches = forward(layers, params, x, m=m, seed=seed, step=step)
-    loss, dy = mse(y, t)
+    loss, dy = loss_fn(layers, y, t)
     dx, grads = backward(layers, params, caches, dy)
     new = [np.asarray(p, np.float64) - lr * g for p, g in zip(params, grads)]
     return dict(loss=loss, y=y, dy=dy, grads=grads, params=new, dx=dx if want_dx else None,

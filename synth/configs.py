@@ -10,6 +10,10 @@ A model is a list of layer dicts.  Keys:
   stash       route id whose skip tensor is this layer's OUTPUT, or -1
   pop         route id consumed (concatenated after x) at this layer's INPUT, or -1
   d_skip      width of the popped skip tensor ("merge" only), else 0
+  n_heads     attention heads ("transformer"), seq: tokens per sample ("embed", "transformer"),
+  vocab       vocabulary size ("embed": d_in = 1, the token id; "lmhead": d_out = vocab)
+  GPT-2-shaped kinds (C5): "embed", "transformer" (pre-LN block, MLP d_hidden, GELU,
+  causal attention), "lmhead" (final LN + untied vocabulary projection, no bias)
 
 A run is described by `Config` (layers + batch + m + n + checkpoint + dtype + lr).
 Nothing here computes anything of the method; it is data only.
@@ -18,9 +22,11 @@ from dataclasses import dataclass, field
 from typing import List, Optional
 
 
-def layer(kind, d_in, d_out, d_hidden=0, act="none", dropout=0.0, stash=-1, pop=-1, d_skip=0):
+def layer(kind, d_in, d_out, d_hidden=0, act="none", dropout=0.0, stash=-1, pop=-1, d_skip=0,
+          n_heads=0, seq=0, vocab=0):
     return dict(kind=kind, d_in=int(d_in), d_out=int(d_out), d_hidden=int(d_hidden), act=act,
-                dropout=float(dropout), stash=int(stash), pop=int(pop), d_skip=int(d_skip))
+                dropout=float(dropout), stash=int(stash), pop=int(pop), d_skip=int(d_skip),
+                n_heads=int(n_heads), seq=int(seq), vocab=int(vocab))
 
 
 @dataclass
@@ -72,6 +78,22 @@ def umlp(d=2048, levels=4, blocks_per_level=2, mid_blocks=2, dropout=0.0):
     return L
 
 
+def gpt2_stack(n_layers=48, d=1600, n_heads=25, seq=1024, vocab=50257, dropout=0.1):
+    """C5 (configs[4]): embed + n_layers pre-LN GPT-2 blocks (MLP 4d, GELU) + final LN / LM head."""
+    L = [layer("embed", 1, d, dropout=dropout, seq=seq, vocab=vocab)]
+    for _ in range(n_layers):
+        L.append(layer("transformer", d, d, d_hidden=4 * d, act="gelu", dropout=dropout,
+                       n_heads=n_heads, seq=seq))
+    L.append(layer("lmhead", d, vocab, vocab=vocab))
+    return L
+
+
+def C5_small(n=2, m=4, checkpoint="always", dropout=0.1, batch=8):
+    """Shrunk C5 (SURVEY 8(c) pins): 4 blocks, d = 128, 2 heads, seq 64, V = 512, B = 8 seqs."""
+    return Config("C5s", gpt2_stack(4, 128, 2, 64, 512, dropout), batch=batch, m=m, n=n,
+                  checkpoint=checkpoint, dtype="bf16", lr=0.01)
+
+
 def bn_mlp(n=4, d=256):
     """BN micro-config: n x [Linear(d->d), BatchNorm(d), ReLU]."""
     L = []
@@ -104,6 +126,10 @@ def BN(m=4, n=2):
 def param_shapes(layers):
     """Parameter tensors in canonical order (layer order; within a layer the order below).
 
+    embed:     wte [vocab, d], wpe [seq, d]
+    transformer: ln1 gamma, beta [d], Wqkv [3d, d], bqkv [3d], Wo [d, d], bo [d], ln2 gamma, beta [d],
+               W1 [d_hidden, d], b1 [d_hidden], W2 [d, d_hidden], b2 [d]
+    lmhead:    gamma [d], beta [d], W [vocab, d]
     linear:    W [d_out, d_in], b [d_out]
     merge:     W [d_out, d_in + d_skip], b [d_out]
     resmlp:    gamma [d_in], beta [d_in], W1 [d_hidden, d_in], b1 [d_hidden], W2 [d_out, d_hidden], b2 [d_out]
@@ -123,6 +149,15 @@ def param_shapes(layers):
                     (li, "W2", (L["d_out"], h)), (li, "b2", (L["d_out"],))]
         elif k == "batchnorm":
             out += [(li, "gamma", (L["d_in"],)), (li, "beta", (L["d_in"],))]
+        elif k == "embed":
+            out += [(li, "wte", (L["vocab"], L["d_out"])), (li, "wpe", (L["seq"], L["d_out"]))]
+        elif k == "transformer":
+            d, h = L["d_in"], L["d_hidden"]
+            out += [(li, "gamma", (d,)), (li, "beta", (d,)), (li, "Wqkv", (3 * d, d)), (li, "bqkv", (3 * d,)),
+                    (li, "Wo", (d, d)), (li, "bo", (d,)), (li, "gamma", (d,)), (li, "beta", (d,)),
+                    (li, "W1", (h, d)), (li, "b1", (h,)), (li, "W2", (d, h)), (li, "b2", (d,))]
+        elif k == "lmhead":
+            out += [(li, "gamma", (L["d_in"],)), (li, "beta", (L["d_in"],)), (li, "W", (L["d_out"], L["d_in"]))]
         else:
             raise ValueError(k)
     return out

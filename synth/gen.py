@@ -30,7 +30,14 @@ def round_bf16(a):
 
 
 def inputs(layers, batch, seed=1234, dtype="fp32"):
-    """Return (x, t) float32 arrays [batch, d_in] and [batch, d_out]."""
+    """Return (x, t) float32 arrays [batch, d_in] and [batch, d_out].  GPT-2-shaped models (first
+    layer "embed"): batch = sequences; x = token ids U{0..V-1} as float32 [batch*seq, 1],
+    t = next-token targets int32 [batch*seq] (also U{0..V-1}; synthetic, no data)."""
+    if layers[0]["kind"] == "embed":
+        V, seq = layers[0]["vocab"], layers[0]["seq"]
+        x = rng(seed, TID_X).integers(0, V, size=(batch * seq, 1)).astype(np.float32)
+        t = rng(seed, TID_T).integers(0, V, size=(batch * seq,)).astype(np.int32)
+        return x, t
     d_in, d_out = layers[0]["d_in"], layers[-1]["d_out"]
     x = rng(seed, TID_X).standard_normal((batch, d_in)).astype(np.float32)
     t = rng(seed, TID_T).standard_normal((batch, d_out)).astype(np.float32)
@@ -44,8 +51,10 @@ def params(layers, seed=1234, dtype="fp32"):
     out = []
     for pid, (li, name, shape) in enumerate(param_shapes(layers)):
         g = rng(seed, TID_PARAM0 + pid)
-        if name in ("W", "W1", "W2", "b", "b1", "b2"):
-            if name in ("b", "b1", "b2"):
+        if name in ("wte", "wpe"):
+            a = g.standard_normal(shape)
+        elif name in ("W", "W1", "W2", "b", "b1", "b2", "Wqkv", "bqkv", "Wo", "bo"):
+            if name in ("b", "b1", "b2", "bqkv", "bo"):
                 fan_in = _fan_in(layers[li], name)
             else:
                 fan_in = shape[1]
@@ -65,6 +74,8 @@ def params(layers, seed=1234, dtype="fp32"):
 
 
 def _fan_in(L, name):
+    if L["kind"] == "transformer":
+        return L["d_hidden"] if name == "b2" else L["d_in"]
     if L["kind"] == "resmlp":
         return L["d_in"] if name == "b1" else L["d_hidden"]
     if L["kind"] == "merge":
