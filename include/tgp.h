@@ -57,8 +57,31 @@ typedef enum { TGP_FP32 = 0, TGP_BF16 = 1 } tgp_dtype;
  *  TGP_BATCHNORM y = act(gamma (x - mu_i) / sqrt(var_i + 1e-5) + beta), statistics of micro-batch i
  *                (P:56 footnote); running stats committed once per forward call from the whole
  *                mini-batch (momentum 0.1, unbiased variance).   gamma [d], beta [d]   (FP32 mode only)
+ *
+ * GPT-2-shaped kinds (C5; BASELINE.json configs[4]; bf16 mode only).  Rows are TOKENS:
+ * a sample is a sequence of `seq` tokens, B counts tokens and must be a multiple of seq, and the
+ * micro-batches split the SEQUENCES (reading Z7 applied to samples), so attention never crosses one.
+ *  TGP_EMBED       y = wte[id] + wpe[row % seq] [dropout, site = layer]; d_in = 1: column 0 of the
+ *                  input holds the token id as an exactly representable fp32 integer.  Must be layer 0.
+ *                  wte [vocab][d_out], wpe [seq][d_out]
+ *  TGP_TRANSFORMER pre-LN GPT-2 block, d = 64 n_heads, MLP d_hidden with GELU, causal attention:
+ *                  x1 = x + drop(Attn(LN1(x)) Wo^T + bo), y = x1 + drop(GELU(LN2(x1) W1^T + b1) W2^T + b2),
+ *                  dropout (p = `dropout`) on the attention probabilities (site layer + 1<<16) and on
+ *                  both residual branches (sites layer + 2<<16, + 3<<16).
+ *                  gamma1 [d], beta1 [d], Wqkv [3d][d], bqkv [3d], Wo [d][d], bo [d], gamma2 [d], beta2 [d],
+ *                  W1 [d_hidden][d], b1 [d_hidden], W2 [d][d_hidden], b2 [d]
+ *  TGP_LMHEAD      logits y = LN(x) W^T (no bias), d_out = vocab.   gamma [d], beta [d], W [vocab][d]
+ * (oracle/model.py states the same formulas; PAPER.md P:25 names GPT-2 as a GPipe workload.)
  */
-typedef enum { TGP_LINEAR = 0, TGP_RESMLP = 1, TGP_MERGE = 2, TGP_BATCHNORM = 3 } tgp_kind;
+typedef enum {
+  TGP_LINEAR = 0,
+  TGP_RESMLP = 1,
+  TGP_MERGE = 2,
+  TGP_BATCHNORM = 3,
+  TGP_EMBED = 4,
+  TGP_TRANSFORMER = 5,
+  TGP_LMHEAD = 6
+} tgp_kind;
 typedef enum { TGP_ACT_NONE = 0, TGP_ACT_RELU = 1, TGP_ACT_GELU = 2 } tgp_act;
 
 typedef struct {
@@ -70,6 +93,9 @@ typedef struct {
                           (seed, step), counter = (global element index >> 2, layer index, step) */
   int32_t stash_route; /* route id whose skip tensor is this layer's OUTPUT, or -1 (@skippable stash) */
   int32_t pop_route;   /* route id consumed at this layer's INPUT (TGP_MERGE), or -1 (pop) */
+  int32_t n_heads;     /* TGP_TRANSFORMER: attention heads (head dim 64), else 0 */
+  int32_t seq;         /* TGP_EMBED / TGP_TRANSFORMER: tokens per sample (multiple of 64), else 0 */
+  int32_t vocab;       /* TGP_EMBED / TGP_LMHEAD: vocabulary size (multiple of 128 for the LM head), else 0 */
 } tgp_layer;
 
 typedef struct tgp_ctx tgp_ctx;
@@ -142,6 +168,13 @@ tgp_status tgp_forward(tgp_ctx* ctx, const float* x, int32_t B, float* y);
  * loss = sum (y - t)^2 / (B d_out), dy = 2 (y - t) / (B d_out).  loss_out: host, may be NULL. */
 tgp_status tgp_mse_loss_grad(tgp_ctx* ctx, const float* y, const float* target, int32_t B, float* dy,
                              double* loss_out);
+
+/* Token cross-entropy on the gathered logits (C5; loss "on the gathered output"):
+ * loss = mean_r (logsumexp(y_r) - y_r[target_r]), dy = (softmax(y_r) - onehot(target_r)) / B.
+ * y, dy: [B][vocab] fp32, target: [B] int32 token ids, all device memory on devices[n-1];
+ * loss_out: host, may be NULL.  Deterministic (fixed-order reductions). */
+tgp_status tgp_ce_loss_grad(tgp_ctx* ctx, const float* y, const int32_t* target, int32_t B, float* dy,
+                            double* loss_out);
 
 /* Backward pass: mirrored clock-cycle, F'_{i,j} before B_{i,j} for checkpointed micro-batches,
  * then the deferred weight-gradient task W_j.  dy: [B][d_out] fp32 on devices[n-1] (iff local);

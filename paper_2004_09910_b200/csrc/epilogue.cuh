@@ -36,7 +36,7 @@ TGP_DEV EpiPre epi_load(const EpiParams& e, int f, int r) {
   } else if constexpr (MODE == EPI_ACT_BWD) {
     if (e.act) q.a = e.zbuf[(int64_t)r * e.ldz + f];
   }
-  if constexpr (MODE == EPI_LINEAR_FWD || MODE == EPI_ACT_BWD) {
+  if constexpr (MODE == EPI_LINEAR_FWD || MODE == EPI_ACT_BWD || MODE == EPI_RESID_FWD) {
     if (e.drop_thresh) {
       const uint64_t idx = (uint64_t)(e.row_global0 + r) * (uint64_t)e.drop_width + (uint64_t)f;
       q.keep = dropout_keep(e.seed, *e.step, e.site, idx, e.drop_thresh);
@@ -58,7 +58,9 @@ TGP_DEV float epi_finish(const EpiParams& e, int f, int r, float v, const EpiPre
     if (e.op) store_op(e, r, f, y);
     return 0.0f;
   } else if constexpr (MODE == EPI_RESID_FWD) {
-    const float y = v + q.a + q.b;
+    float br = v + q.a;  // residual branch (dropout on the branch: GPT-2 blocks)
+    if (e.drop_thresh) br = q.keep ? br * e.drop_scale : 0.0f;
+    const float y = br + q.b;
     e.out0[(int64_t)r * e.ld0 + f] = y;
     if (e.op) store_op(e, r, f, y);
     return 0.0f;

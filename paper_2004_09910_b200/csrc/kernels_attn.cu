@@ -1,0 +1,563 @@
+// GPT-2-shaped stage kernels (C5, BASELINE.json configs[4]): causal multi-head
+// attention forward / backward, token + position embedding forward and its deterministic deferred
+// weight gradient, and the token cross-entropy loss.  The formulas are the textbook ones the oracle
+// states (oracle/model.py header; reading Z13); dropout uses the same Philox decision as every other
+// site (O8), on the [n_seq, n_heads, seq, seq] probability tensor for attention.
+//
+// Attention: head dim 64, 64-row query / key tiles, one CTA of 4 warps per (tile, head, sequence),
+// bf16 mma.sync m16n8k16 with fp32 accumulation (the tiles are 64 x 64: too small for a 128-row
+// tcgen05 MMA per warp group), flash-style online softmax.  Backward recomputes P
+// from the saved log-sum-exp and splits into a dK/dV kernel (per key tile, loop over query tiles)
+// and a dQ kernel (per query tile, loop over key tiles): every output element is written by exactly
+// one thread, no atomics, so the backward is deterministic.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "host.h"
+#include "kernels_gpt.h"
+
+namespace tgp {
+
+namespace {
+
+constexpr int HD = 64;     // head dim
+constexpr int TILE = 64;   // query / key tile
+constexpr int PITCH = 72;  // smem row pitch (bf16 elements): conflict-free fragment loads
+constexpr float LOG2E = 1.4426950408889634f;
+
+TGP_DEV void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+TGP_DEV uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+TGP_DEV uint32_t ld32(const __nv_bfloat16* p) { return *reinterpret_cast<const uint32_t*>(p); }
+
+// 64 rows x 64 bf16 columns from global (row stride ld elements) into smem [64][PITCH]; optionally
+// also the transpose into smem T[64][PITCH] (T[c][r] = X[r][c]).
+TGP_DEV void load_tile(const __nv_bfloat16* g, int64_t ld, __nv_bfloat16* S, __nv_bfloat16* T) {
+  for (int q = threadIdx.x; q < TILE * 8; q += blockDim.x) {
+    const int r = q >> 3, c8 = (q & 7) * 8;
+    const uint4 v = *reinterpret_cast<const uint4*>(g + (int64_t)r * ld + c8);
+    if (S) *reinterpret_cast<uint4*>(S + r * PITCH + c8) = v;
+    if (T) {
+      const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) T[(c8 + k) * PITCH + r] = e[k];
+    }
+  }
+}
+// same from fp32 global (converted to bf16)
+TGP_DEV void load_tile_f32(const float* g, int64_t ld, __nv_bfloat16* S, __nv_bfloat16* T) {
+  for (int q = threadIdx.x; q < TILE * 16; q += blockDim.x) {
+    const int r = q >> 4, c4 = (q & 15) * 4;
+    const float4 v = *reinterpret_cast<const float4*>(g + (int64_t)r * ld + c4);
+    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __nv_bfloat16 b = __float2bfloat16_rn(e[k]);
+      if (S) S[r * PITCH + c4 + k] = b;
+      if (T) T[(c4 + k) * PITCH + r] = b;
+    }
+  }
+}
+// A fragments (16 rows starting at row0, k = 64) of a [64][PITCH] smem tile
+TGP_DEV void load_afrag(const __nv_bfloat16* S, int row0, uint32_t (*a)[4]) {
+  const int g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc) {
+    a[kc][0] = ld32(S + (row0 + g) * PITCH + kc * 16 + 2 * t);
+    a[kc][1] = ld32(S + (row0 + g + 8) * PITCH + kc * 16 + 2 * t);
+    a[kc][2] = ld32(S + (row0 + g) * PITCH + kc * 16 + 8 + 2 * t);
+    a[kc][3] = ld32(S + (row0 + g + 8) * PITCH + kc * 16 + 8 + 2 * t);
+  }
+}
+// acc[nt][4] (+)= A(16 x 64, fragments a) * B^T, B element (n, k) = Bs[n][k] for n < 64
+TGP_DEV void mma_row_tile(float (*acc)[4], const uint32_t (*a)[4], const __nv_bfloat16* Bs) {
+  const int g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc)
+      mma16816(acc[nt], a[kc], ld32(Bs + (nt * 8 + g) * PITCH + kc * 16 + 2 * t),
+               ld32(Bs + (nt * 8 + g) * PITCH + kc * 16 + 8 + 2 * t));
+}
+// acc[dt][4] += P(16 x 64 from accumulator layout p[nt][4]) * X, X element (k, n) = Xt[n][k]
+TGP_DEV void mma_p_tile(float (*acc)[4], const float (*p)[4], const __nv_bfloat16* Xt) {
+  const int g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc) {
+    uint32_t a[4];
+    a[0] = pack2(p[2 * kc][0], p[2 * kc][1]);
+    a[1] = pack2(p[2 * kc][2], p[2 * kc][3]);
+    a[2] = pack2(p[2 * kc + 1][0], p[2 * kc + 1][1]);
+    a[3] = pack2(p[2 * kc + 1][2], p[2 * kc + 1][3]);
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt)
+      mma16816(acc[dt], a, ld32(Xt + (dt * 8 + g) * PITCH + kc * 16 + 2 * t),
+               ld32(Xt + (dt * 8 + g) * PITCH + kc * 16 + 8 + 2 * t));
+  }
+}
+
+struct AttnArgs {
+  const __nv_bfloat16* qkv;  // [rows][3d] (q | k | v), rows pre-offset to the micro-batch
+  int64_t ldq;
+  int d, nh, seq;
+  int64_t seq0;  // global sequence index of row 0 (dropout counters)
+  float scale_log2;  // log2(e) / sqrt(64)
+  float scale;       // 1 / sqrt(64)
+  uint32_t thresh;
+  float dscale;
+  uint64_t seed;
+  const uint32_t* step;
+  uint32_t site;
+};
+
+TGP_DEV bool attn_keep(const AttnArgs& A, int s, int h, int q, int k) {
+  const uint64_t idx = (((uint64_t)(A.seq0 + s) * A.nh + h) * A.seq + q) * A.seq + k;
+  return dropout_keep(A.seed, *A.step, A.site, idx, A.thresh);
+}
+
+__global__ void __launch_bounds__(128) attn_fwd_kernel(AttnArgs A, __nv_bfloat16* __restrict__ ctx, int64_t ldc,
+                                                       float* __restrict__ lse) {
+  __shared__ __align__(16) __nv_bfloat16 Qs[TILE * PITCH], Ks[TILE * PITCH], Vt[TILE * PITCH];
+  const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+  const int w = threadIdx.x >> 5, g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
+  const int64_t base = (int64_t)s * A.seq;
+  load_tile(A.qkv + (base + qt * TILE) * A.ldq + h * HD, A.ldq, Qs, nullptr);
+  __syncthreads();
+  uint32_t qa[4][4];
+  load_afrag(Qs, w * 16, qa);
+  float m2[2] = {-INFINITY, -INFINITY}, l[2] = {0.0f, 0.0f};
+  float o[8][4] = {};
+  const int q0 = qt * TILE + w * 16 + g;
+  for (int kt = 0; kt <= qt; ++kt) {
+    __syncthreads();
+    load_tile(A.qkv + (base + kt * TILE) * A.ldq + A.d + h * HD, A.ldq, Ks, nullptr);
+    load_tile(A.qkv + (base + kt * TILE) * A.ldq + 2 * A.d + h * HD, A.ldq, nullptr, Vt);
+    __syncthreads();
+    float sc[8][4] = {};
+    mma_row_tile(sc, qa, Ks);
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int key = kt * TILE + nt * 8 + 2 * t + (c & 1), q = q0 + (c >> 1) * 8;
+        float v = sc[nt][c] * A.scale_log2;
+        if (key > q) v = -INFINITY;
+        sc[nt][c] = v;
+        mx[c >> 1] = fmaxf(mx[c >> 1], v);
+      }
+    float alpha[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      const float mn = fmaxf(m2[r], mx[r]);
+      alpha[r] = exp2f(m2[r] - mn);
+      m2[r] = mn;
+      l[r] *= alpha[r];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float p = exp2f(sc[nt][c] - m2[c >> 1]);
+        l[c >> 1] += p;
+        if (A.thresh) {
+          const int key = kt * TILE + nt * 8 + 2 * t + (c & 1), q = q0 + (c >> 1) * 8;
+          p = (key <= q && attn_keep(A, s, h, q, key)) ? p * A.dscale : 0.0f;
+        }
+        sc[nt][c] = p;
+      }
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+      o[dt][0] *= alpha[0];
+      o[dt][1] *= alpha[0];
+      o[dt][2] *= alpha[1];
+      o[dt][3] *= alpha[1];
+    }
+    mma_p_tile(o, sc, Vt);
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    l[r] += __shfl_xor_sync(0xffffffffu, l[r], 1);
+    l[r] += __shfl_xor_sync(0xffffffffu, l[r], 2);
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int64_t row = base + q0 + r * 8;
+    const float inv = 1.0f / l[r];
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt)
+      *reinterpret_cast<uint32_t*>(ctx + row * ldc + h * HD + dt * 8 + 2 * t) =
+          pack2(o[dt][2 * r] * inv, o[dt][2 * r + 1] * inv);
+    if (t == 0) lse[row * A.nh + h] = m2[r] + log2f(l[r]);  // log2 domain
+  }
+}
+
+// D[row][h] = sum_c dO[row][h*64 + c] * O[row][h*64 + c]  (= rowsum(P o dP), the softmax VJP term)
+__global__ void attn_bwd_prep_kernel(const float* __restrict__ dO, const __nv_bfloat16* __restrict__ O, int64_t ld,
+                                     int rows, int nh, float* __restrict__ D) {
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= rows * nh) return;
+  const int r = wid / nh, h = wid % nh;
+  const float2 a = *reinterpret_cast<const float2*>(dO + (int64_t)r * ld + h * HD + 2 * lane);
+  const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(O + (int64_t)r * ld + h * HD + 2 * lane);
+  float v = a.x * __low2float(b) + a.y * __high2float(b);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) D[wid] = v;
+}
+
+// dK, dV of one key tile: loop over the query tiles at or after it.
+__global__ void __launch_bounds__(128) attn_bwd_dkv_kernel(AttnArgs A, const float* __restrict__ dO, int64_t ldo,
+                                                           const float* __restrict__ lse, const float* __restrict__ D,
+                                                           float* __restrict__ dqkv, int64_t ldg) {
+  __shared__ __align__(16) __nv_bfloat16 Qs[TILE * PITCH], Qt[TILE * PITCH], Os[TILE * PITCH], Ot[TILE * PITCH];
+  __shared__ float ls[TILE], Ds[TILE];
+  const int kt = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+  const int w = threadIdx.x >> 5, g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
+  const int64_t base = (int64_t)s * A.seq;
+  const int nq = A.seq / TILE;
+  load_tile(A.qkv + (base + kt * TILE) * A.ldq + A.d + h * HD, A.ldq, Qs, nullptr);
+  load_tile(A.qkv + (base + kt * TILE) * A.ldq + 2 * A.d + h * HD, A.ldq, Os, nullptr);
+  __syncthreads();
+  uint32_t ka[4][4], va[4][4];
+  load_afrag(Qs, w * 16, ka);
+  load_afrag(Os, w * 16, va);
+  float dk[8][4] = {}, dv[8][4] = {};
+  const int k0 = kt * TILE + w * 16 + g;
+  for (int qt = kt; qt < nq; ++qt) {
+    __syncthreads();
+    load_tile(A.qkv + (base + qt * TILE) * A.ldq + h * HD, A.ldq, Qs, Qt);
+    load_tile_f32(dO + (base + qt * TILE) * ldo + h * HD, ldo, Os, Ot);
+    if (threadIdx.x < TILE) {
+      ls[threadIdx.x] = lse[(base + qt * TILE + threadIdx.x) * A.nh + h];
+      Ds[threadIdx.x] = D[(base + qt * TILE + threadIdx.x) * A.nh + h];
+    }
+    __syncthreads();
+    float p[8][4] = {}, dp[8][4] = {};
+    mma_row_tile(p, ka, Qs);   // S^T[key][q]
+    mma_row_tile(dp, va, Os);  // dP^T[key][q] = V dO^T
+    float pd[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int ql = nt * 8 + 2 * t + (c & 1), q = qt * TILE + ql, key = k0 + (c >> 1) * 8;
+        const float pr = key <= q ? exp2f(p[nt][c] * A.scale_log2 - ls[ql]) : 0.0f;
+        float dpv = dp[nt][c];
+        float pdv = pr;
+        if (A.thresh) {
+          const bool keep = key <= q && attn_keep(A, s, h, q, key);
+          pdv = keep ? pr * A.dscale : 0.0f;
+          dpv = keep ? dpv * A.dscale : 0.0f;
+        }
+        pd[nt][c] = pdv;
+        p[nt][c] = pr * (dpv - Ds[ql]);  // dS^T
+      }
+    mma_p_tile(dv, pd, Ot);  // dV += Pd^T dO
+    mma_p_tile(dk, p, Qt);   // dK += dS^T Q
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int64_t row = base + k0 + r * 8;
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+      const int col = h * HD + dt * 8 + 2 * t;
+      *reinterpret_cast<float2*>(dqkv + row * ldg + A.d + col) =
+          make_float2(dk[dt][2 * r] * A.scale, dk[dt][2 * r + 1] * A.scale);
+      *reinterpret_cast<float2*>(dqkv + row * ldg + 2 * A.d + col) = make_float2(dv[dt][2 * r], dv[dt][2 * r + 1]);
+    }
+  }
+}
+
+// dQ of one query tile: loop over the key tiles at or before it.
+__global__ void __launch_bounds__(128) attn_bwd_dq_kernel(AttnArgs A, const float* __restrict__ dO, int64_t ldo,
+                                                          const float* __restrict__ lse, const float* __restrict__ D,
+                                                          float* __restrict__ dqkv, int64_t ldg) {
+  __shared__ __align__(16) __nv_bfloat16 Ks[TILE * PITCH], Kt[TILE * PITCH], Vs[TILE * PITCH];
+  const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+  const int w = threadIdx.x >> 5, g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
+  const int64_t base = (int64_t)s * A.seq;
+  load_tile(A.qkv + (base + qt * TILE) * A.ldq + h * HD, A.ldq, Ks, nullptr);
+  load_tile_f32(dO + (base + qt * TILE) * ldo + h * HD, ldo, Vs, nullptr);
+  __syncthreads();
+  uint32_t qa[4][4], oa[4][4];
+  load_afrag(Ks, w * 16, qa);
+  load_afrag(Vs, w * 16, oa);
+  const int q0 = qt * TILE + w * 16 + g;
+  float ls[2], Dr[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    ls[r] = lse[(base + q0 + r * 8) * A.nh + h];
+    Dr[r] = D[(base + q0 + r * 8) * A.nh + h];
+  }
+  float dq[8][4] = {};
+  for (int kt = 0; kt <= qt; ++kt) {
+    __syncthreads();
+    load_tile(A.qkv + (base + kt * TILE) * A.ldq + A.d + h * HD, A.ldq, Ks, Kt);
+    load_tile(A.qkv + (base + kt * TILE) * A.ldq + 2 * A.d + h * HD, A.ldq, Vs, nullptr);
+    __syncthreads();
+    float p[8][4] = {}, dp[8][4] = {};
+    mma_row_tile(p, qa, Ks);   // S
+    mma_row_tile(dp, oa, Vs);  // dP = dO V^T
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int key = kt * TILE + nt * 8 + 2 * t + (c & 1), q = q0 + (c >> 1) * 8;
+        const float pr = key <= q ? exp2f(p[nt][c] * A.scale_log2 - ls[c >> 1]) : 0.0f;
+        float dpv = dp[nt][c];
+        if (A.thresh) dpv = (key <= q && attn_keep(A, s, h, q, key)) ? dpv * A.dscale : 0.0f;
+        p[nt][c] = pr * (dpv - Dr[c >> 1]);  // dS
+      }
+    mma_p_tile(dq, p, Kt);  // dQ += dS K
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int64_t row = base + q0 + r * 8;
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt)
+      *reinterpret_cast<float2*>(dqkv + row * ldg + h * HD + dt * 8 + 2 * t) =
+          make_float2(dq[dt][2 * r] * A.scale, dq[dt][2 * r + 1] * A.scale);
+  }
+}
+
+AttnArgs make_args(const void* qkv, int rows, int d, int nh, int seq, int64_t row_global0, uint32_t thresh,
+                   float dscale, uint64_t seed, const uint32_t* step, uint32_t site) {
+  AttnArgs A;
+  A.qkv = (const __nv_bfloat16*)qkv;
+  A.ldq = 3 * (int64_t)d;
+  A.d = d;
+  A.nh = nh;
+  A.seq = seq;
+  A.seq0 = row_global0 / seq;
+  A.scale = 0.125f;
+  A.scale_log2 = 0.125f * LOG2E;
+  A.thresh = thresh;
+  A.dscale = dscale;
+  A.seed = seed;
+  A.step = step;
+  A.site = site;
+  (void)rows;
+  return A;
+}
+
+
+// ------------------------------------------------------------------------------- embedding
+__global__ void embed_fwd_kernel(const float* __restrict__ ids, int64_t ldi, const float* __restrict__ wte,
+                                 const float* __restrict__ wpe, int d, int seq, int64_t row_global0, uint32_t thresh,
+                                 float dscale, uint64_t seed, const uint32_t* step, uint32_t site, float* __restrict__ y) {
+  const int r = blockIdx.x;
+  const int64_t id = (int64_t)__float2int_rn(ids[(int64_t)r * ldi]);
+  const int64_t pos = (row_global0 + r) % seq;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float v = wte[id * d + c] + wpe[pos * d + c];
+    if (thresh) v = dropout_keep(seed, *step, site, (uint64_t)(row_global0 + r) * d + c, thresh) ? v * dscale : 0.0f;
+    y[(int64_t)r * d + c] = v;
+  }
+}
+
+// deterministic dW_te: counting sort of the token rows by id, each vocabulary row sums its rows in
+// ascending order (no floating-point atomics)
+__global__ void embed_count_kernel(const float* __restrict__ ids, int64_t ldi, int rows, int* cnt) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    atomicAdd(cnt + __float2int_rn(ids[(int64_t)r * ldi]), 1);
+}
+__global__ void embed_scan_kernel(const int* __restrict__ cnt, int V, int* start, int* cursor) {
+  __shared__ int tot[1024];
+  const int per = (V + blockDim.x - 1) / blockDim.x;
+  const int a = threadIdx.x * per, b = min(V, a + per);
+  int s = 0;
+  for (int v = a; v < b; ++v) s += cnt[v];
+  tot[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const int x = tot[i];
+      tot[i] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+  int run = tot[threadIdx.x];
+  for (int v = a; v < b; ++v) {
+    start[v] = run;
+    cursor[v] = run;
+    run += cnt[v];
+  }
+}
+__global__ void embed_fill_kernel(const float* __restrict__ ids, int64_t ldi, int rows, int* cursor, int* list) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    list[atomicAdd(cursor + __float2int_rn(ids[(int64_t)r * ldi]), 1)] = r;
+}
+// one CTA per vocabulary row: sort its bucket (ascending row), sum the rows
+__global__ void embed_wte_kernel(const int* __restrict__ cnt, const int* __restrict__ start, int* list,
+                                 const float* __restrict__ dE, int d, float* __restrict__ dwte, int accumulate) {
+  const int v = blockIdx.x, n = cnt[v];
+  int* L = list + start[v];
+  if (threadIdx.x == 0)
+    for (int i = 1; i < n; ++i) {  // insertion sort (buckets hold ~B/V rows)
+      const int x = L[i];
+      int j = i - 1;
+      while (j >= 0 && L[j] > x) {
+        L[j + 1] = L[j];
+        --j;
+      }
+      L[j + 1] = x;
+    }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float s = accumulate ? dwte[(int64_t)v * d + c] : 0.0f;
+    for (int i = 0; i < n; ++i) s += dE[(int64_t)L[i] * d + c];
+    dwte[(int64_t)v * d + c] = s;
+  }
+}
+__global__ void embed_wpe_kernel(const float* __restrict__ dE, int rows, int d, int seq, float* __restrict__ dwpe,
+                                 int accumulate) {
+  const int p = blockIdx.x;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float s = accumulate ? dwpe[(int64_t)p * d + c] : 0.0f;
+    for (int r = p; r < rows; r += seq) s += dE[(int64_t)r * d + c];
+    dwpe[(int64_t)p * d + c] = s;
+  }
+}
+
+// ------------------------------------------------------------------------------- cross-entropy
+__global__ void ce_row_kernel(const float* __restrict__ y, int64_t ldy, const int* __restrict__ tgt, int V, int T,
+                              float* __restrict__ dy, double* __restrict__ part) {
+  __shared__ float sh[32];
+  __shared__ float bc;
+  const int r = blockIdx.x;
+  const float* yr = y + (int64_t)r * ldy;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, yr[c]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) sh[w] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = sh[0];
+    for (int i = 1; i < nw; ++i) m = fmaxf(m, sh[i]);
+    bc = m;
+  }
+  __syncthreads();
+  mx = bc;
+  float se = 0.0f;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) se += __expf(yr[c] - mx);
+  for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+  __syncthreads();
+  if (lane == 0) sh[w] = se;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.0f;
+    for (int i = 0; i < nw; ++i) s += sh[i];  // fixed order
+    bc = s;
+  }
+  __syncthreads();
+  se = bc;
+  const int tg = tgt[r];
+  const float inv = 1.0f / se, invT = 1.0f / (float)T;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    const float p = __expf(yr[c] - mx) * inv;
+    dy[(int64_t)r * ldy + c] = (p - (c == tg ? 1.0f : 0.0f)) * invT;
+  }
+  if (threadIdx.x == 0) part[r] = (double)mx + log((double)se) - (double)yr[tg];
+}
+__global__ void ce_final_kernel(const double* part, int T, double* loss) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < T; ++i) s += part[i];
+    loss[0] = s / (double)T;
+  }
+}
+
+template <typename Kern, typename... Args>
+int launch(const char* name, Kern k, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  k<<<grid, block, 0, st>>>(args...);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s launch: %s", name, cudaGetErrorString(e));
+    return -3;
+  }
+  return 0;
+}
+
+}  // namespace
+
+bool attn_shape_ok(int rows, int d, int nh, int seq) {
+  return nh > 0 && d == nh * HD && seq % TILE == 0 && seq > 0 && rows % seq == 0;
+}
+
+int attn_fwd(cudaStream_t st, const void* qkv, int rows, int d, int nh, int seq, int64_t row_global0,
+             uint32_t thresh, float dscale, uint64_t seed, const uint32_t* step, uint32_t site, void* ctx,
+             float* lse) {
+  if (!attn_shape_ok(rows, d, nh, seq)) {
+    set_error("attention: need d = 64 * n_heads, seq %% 64 == 0, rows %% seq == 0 (d=%d nh=%d seq=%d rows=%d)", d,
+              nh, seq, rows);
+    return TGP_E_UNSUPPORTED;
+  }
+  AttnArgs A = make_args(qkv, rows, d, nh, seq, row_global0, thresh, dscale, seed, step, site);
+  return launch("attn_fwd", attn_fwd_kernel, dim3(seq / TILE, nh, rows / seq), dim3(128), st, A,
+                (__nv_bfloat16*)ctx, (int64_t)d, lse);
+}
+
+int attn_bwd(cudaStream_t st, const void* qkv, const void* ctx, const float* dO, const float* lse, float* Dbuf,
+             int rows, int d, int nh, int seq, int64_t row_global0, uint32_t thresh, float dscale, uint64_t seed,
+             const uint32_t* step, uint32_t site, float* dqkv) {
+  if (!attn_shape_ok(rows, d, nh, seq)) {
+    set_error("attention backward: unsupported shape");
+    return TGP_E_UNSUPPORTED;
+  }
+  AttnArgs A = make_args(qkv, rows, d, nh, seq, row_global0, thresh, dscale, seed, step, site);
+  const int warps = rows * nh;
+  TGP_TRY(launch("attn_bwd_prep", attn_bwd_prep_kernel, dim3((warps + 3) / 4), dim3(128), st, dO,
+                 (const __nv_bfloat16*)ctx, (int64_t)d, rows, nh, Dbuf));
+  TGP_TRY(launch("attn_bwd_dkv", attn_bwd_dkv_kernel, dim3(seq / TILE, nh, rows / seq), dim3(128), st, A, dO,
+                 (int64_t)d, lse, (const float*)Dbuf, dqkv, 3 * (int64_t)d));
+  return launch("attn_bwd_dq", attn_bwd_dq_kernel, dim3(seq / TILE, nh, rows / seq), dim3(128), st, A, dO, (int64_t)d,
+                lse, (const float*)Dbuf, dqkv, 3 * (int64_t)d);
+}
+
+int embed_fwd(cudaStream_t st, const float* ids, int64_t ldi, int rows, const float* wte, const float* wpe, int d,
+              int seq, int64_t row_global0, uint32_t thresh, float dscale, uint64_t seed, const uint32_t* step,
+              uint32_t site, float* y) {
+  return launch("embed_fwd", embed_fwd_kernel, dim3(rows), dim3(256), st, ids, ldi, wte, wpe, d, seq, row_global0,
+                thresh, dscale, seed, step, site, y);
+}
+
+int embed_wgrad(cudaStream_t st, const float* ids, int64_t ldi, int rows, const float* dE, int d, int V, int seq,
+                int* scratch, float* dwte, float* dwpe, bool accumulate) {
+  int* cnt = scratch;
+  int* start = cnt + V;
+  int* cursor = start + V;
+  int* list = cursor + V;
+  TGP_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)V, st));
+  TGP_TRY(launch("embed_count", embed_count_kernel, dim3(std::min(1024, (rows + 255) / 256)), dim3(256), st, ids,
+                 ldi, rows, cnt));
+  TGP_TRY(launch("embed_scan", embed_scan_kernel, dim3(1), dim3(1024), st, (const int*)cnt, V, start, cursor));
+  TGP_TRY(launch("embed_fill", embed_fill_kernel, dim3(std::min(1024, (rows + 255) / 256)), dim3(256), st, ids, ldi,
+                 rows, cursor, list));
+  TGP_TRY(launch("embed_wte", embed_wte_kernel, dim3(V), dim3(128), st, (const int*)cnt, (const int*)start, list, dE,
+                 d, dwte, (int)accumulate));
+  return launch("embed_wpe", embed_wpe_kernel, dim3(seq), dim3(128), st, dE, rows, d, seq, dwpe, (int)accumulate);
+}
+
+int ce_loss_grad(cudaStream_t st, const float* y, int64_t ldy, const int* tgt, int T, int V, float* dy,
+                 double* part, double* loss_dev) {
+  TGP_TRY(launch("ce_row", ce_row_kernel, dim3(T), dim3(256), st, y, ldy, tgt, V, T, dy, part));
+  return launch("ce_final", ce_final_kernel, dim3(1), dim3(32), st, (const double*)part, T, loss_dev);
+}
+
+}  // namespace tgp

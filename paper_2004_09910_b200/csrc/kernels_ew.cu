@@ -123,7 +123,7 @@ __global__ void ln_bwd_rows_kernel(const float* __restrict__ dh, const float* __
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     const float dn = dhr[c] * gamma[c];
     const float nn = (xr[c] - mu) * rs;
-    dx[(int64_t)r * d + c] = dy[(int64_t)r * d + c] + rs * (dn - m1 - nn * m2);
+    dx[(int64_t)r * d + c] = (dy ? dy[(int64_t)r * d + c] : 0.0f) + rs * (dn - m1 - nn * m2);
   }
 }
 

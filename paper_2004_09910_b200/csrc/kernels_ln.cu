@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(256) ln_bwd_cl_kernel(const float* __restrict_
     const float m1 = gathered_total(gath, 0, rl, CL) / (float)d;
     const float m2 = gathered_total(gath, 1, rl, CL) / (float)d;
     if (r < rows) {
-      const float4 dyv = *reinterpret_cast<const float4*>(dy + (int64_t)r * d + c0);
+      const float4 dyv = dy ? *reinterpret_cast<const float4*>(dy + (int64_t)r * d + c0) : make_float4(0.f, 0.f, 0.f, 0.f);  // dy nullable: no residual
       const float4 n = vn[k], a = vdh[k];
       float4 o;
       o.x = dyv.x + rr[k] * (a.x * g.x - m1 - n.x * m2);

@@ -14,6 +14,7 @@
 
 #include "host.h"
 #include "runtime.h"
+#include "kernels_gpt.h"
 #include "task_stream.h"
 
 using namespace tgp;
@@ -352,6 +353,20 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
 }
 
 // F_{i,j} (and F'_{i,j}: identical kernels and launch configuration -> bitwise identical output)
+// LayerNorm backward dx = dy + LN_bwd(dh) (dy nullable) with the per-16-row column partials.
+static int ln_bwd_any(tgp_ctx* c, Stage& s, bool pdl, const float* dh, const float* x, const float* mean,
+                      const float* rstd, const float* gamma, const float* dy, float* dx, int M, int d, float* pg,
+                      float* pbt) {
+  if (ln_cluster_ok(d)) {
+    TGP_TRY(ln_bwd_cl(s.comp, pdl, dh, x, mean, rstd, gamma, dy, dx, M, d, c->pb, pg, pbt, nullptr, c->bf16, nullptr));
+    c->kernels++;
+  } else {
+    TGP_TRY(ln_bwd(s.comp, pdl, dh, x, mean, rstd, gamma, dy, dx, M, d, pg, pbt));
+    c->kernels += 2;
+  }
+  return 0;
+}
+
 static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
   if (use_stream(c, s, M)) return exec_task_stream(c, s, i, r0, M, false);
   const int slot = c->slot_of[i];
@@ -436,6 +451,90 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         }
         TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 4), dout, H, H}, false, Opnd{L.Gop, c->max_batch, H, H},
                          nullptr, false, dout, M, H, r0, H, true, e2, next_fwd(c, s, l)));
+        break;
+      }
+      case TGP_EMBED: {
+        const float p = L.L.dropout;
+        TGP_TRY(embed_fwd(s.comp, x, s.d_in, M, mparam(s, L, 0), mparam(s, L, 1), dout, L.L.seq, r0, drop_thresh(p),
+                          p > 0 ? 1.0f / (1.0f - p) : 1.0f, c->seed, s.dstep, (uint32_t)l, y));
+        c->kernels++;
+        first_kernel = false;
+        break;
+      }
+      case TGP_LMHEAD: {
+        TGP_TRY(ln_fwd_cl(s.comp, pdl() && c->use_pdl, x, din, M, din, mparam(s, L, 0), mparam(s, L, 1),
+                          opptr(c, L.Hop, r0, din), din, true, L.mean[slot], L.rstd[slot]));
+        c->kernels++;
+        EpiParams e1 = e;
+        e1.mode = EPI_LINEAR_FWD;
+        e1.act = TGP_ACT_NONE;
+        e1.bias = nullptr;
+        e1.out0 = y;
+        e1.ld0 = dout;
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 2), dout, din, din}, false, Opnd{L.Hop, c->max_batch, din, din},
+                         nullptr, false, dout, M, din, r0, din, true, e1));
+        break;
+      }
+      case TGP_TRANSFORMER: {
+        // x1 = x + drop(Attn(LN1(x)) Wo^T + bo); y = x1 + drop(GELU(LN2(x1) W1^T + b1) W2^T + b2)
+        const int d = din, H = L.L.d_hidden, d3 = 3 * din;
+        const float p = L.L.dropout;
+        const uint32_t th = drop_thresh(p);
+        const float dsc = p > 0 ? 1.0f / (1.0f - p) : 1.0f;
+        TGP_TRY(ln_fwd_cl(s.comp, pdl() && c->use_pdl, x, d, M, d, mparam(s, L, 0), mparam(s, L, 1),
+                          opptr(c, L.Hop, r0, d), d, true, L.mean[slot], L.rstd[slot]));
+        c->kernels++;
+        EpiParams e1 = e;
+        e1.mode = EPI_LINEAR_FWD;
+        e1.act = TGP_ACT_NONE;
+        e1.bias = mparam(s, L, 3);
+        e1.op = opptr(c, L.QKVop, r0, d3);
+        e1.ld_op = d3;
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 2), d3, d, d}, false, Opnd{L.Hop, c->max_batch, d, d},
+                         nullptr, false, d3, M, d, r0, d, true, e1));
+        TGP_TRY(attn_fwd(s.comp, opptr(c, L.QKVop, r0, d3), M, d, L.L.n_heads, L.L.seq, r0, th, dsc, c->seed, s.dstep,
+                         (uint32_t)l + (1u << 16), opptr(c, L.CTXop, r0, d), L.lse[slot]));
+        c->kernels++;
+        first_kernel = true;  // the attention kernel does not trigger dependents early
+        EpiParams e2 = e;
+        e2.mode = EPI_RESID_FWD;
+        e2.bias = mparam(s, L, 5);
+        e2.res = x;
+        e2.ld_res = d;
+        e2.out0 = L.x1[slot];
+        e2.ld0 = d;
+        e2.drop_thresh = th;
+        e2.drop_scale = dsc;
+        e2.drop_width = d;
+        e2.site = (uint32_t)l + (2u << 16);
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 4), d, d, d}, false, Opnd{L.CTXop, c->max_batch, d, d},
+                         nullptr, false, d, M, d, r0, d, true, e2));
+        TGP_TRY(ln_fwd_cl(s.comp, pdl() && c->use_pdl, L.x1[slot], d, M, d, mparam(s, L, 6), mparam(s, L, 7),
+                          opptr(c, L.H2op, r0, d), d, true, L.mean2[slot], L.rstd2[slot]));
+        c->kernels++;
+        EpiParams e3 = e;
+        e3.mode = EPI_LINEAR_FWD;
+        e3.act = TGP_ACT_GELU;
+        e3.bias = mparam(s, L, 9);
+        e3.zbuf = L.z[slot];
+        e3.ldz = H;
+        e3.op = opptr(c, L.Gop, r0, H);
+        e3.ld_op = H;
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 8), H, d, d}, false, Opnd{L.H2op, c->max_batch, d, d},
+                         nullptr, false, H, M, d, r0, d, true, e3));
+        EpiParams e4 = e;
+        e4.mode = EPI_RESID_FWD;
+        e4.bias = mparam(s, L, 11);
+        e4.res = L.x1[slot];
+        e4.ld_res = d;
+        e4.out0 = y;
+        e4.ld0 = d;
+        e4.drop_thresh = th;
+        e4.drop_scale = dsc;
+        e4.drop_width = d;
+        e4.site = (uint32_t)l + (3u << 16);
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 10), d, H, H}, false, Opnd{L.Gop, c->max_batch, H, H},
+                         nullptr, false, d, M, H, r0, H, true, e4));
         break;
       }
       case TGP_BATCHNORM: {
@@ -565,6 +664,81 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         }
         break;
       }
+      case TGP_EMBED: {
+        // stash the output gradient (dropout mask applied) for the deferred embedding gradient in W_j
+        const float p = L.L.dropout;
+        TGP_TRY(colwise(s.comp, pdl() && c->use_pdl, g, dout, nullptr, M, dout, 0, drop_thresh(p),
+                        p > 0 ? 1.0f / (1.0f - p) : 1.0f, c->seed, s.dstep, (uint32_t)l, r0,
+                        L.dE + (size_t)r0 * dout, dout, false, nullptr));
+        c->kernels++;
+        dyop_ready = false;
+        break;
+      }
+      case TGP_LMHEAD: {
+        TGP_TRY(colwise(s.comp, pdl() && c->use_pdl, g, dout, nullptr, M, dout, 0, 0u, 1.0f, c->seed, s.dstep,
+                        (uint32_t)l, r0, opptr(c, L.dYop, r0, dout), dout, true, nullptr));
+        c->kernels++;
+        EpiParams e2 = e;
+        e2.mode = EPI_STORE;
+        e2.out0 = s.dh;
+        e2.ld0 = din;
+        e2.split_f = din;
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 2), dout, din, din}, true,
+                         Opnd{L.dYop, c->max_batch, dout, dout}, nullptr, false, din, M, dout, r0, dout, true, e2));
+        TGP_TRY(ln_bwd_any(c, s, pdl() && c->use_pdl, s.dh, xin, L.mean[slot], L.rstd[slot], mparam(s, L, 0), nullptr,
+                           dx, M, din, L.pg + po * din, L.pbt + po * din));
+        dyop_ready = false;
+        break;
+      }
+      case TGP_TRANSFORMER: {
+        const int d = din, H = L.L.d_hidden, d3 = 3 * din;
+        const float p = L.L.dropout;
+        const uint32_t th = drop_thresh(p);
+        const float dsc = p > 0 ? 1.0f / (1.0f - p) : 1.0f;
+        // MLP branch: dm = g o keep3 -> bf16 dY operand (+ b2 partial)
+        TGP_TRY(colwise(s.comp, pdl() && c->use_pdl, g, d, nullptr, M, d, 0, th, dsc, c->seed, s.dstep,
+                        (uint32_t)l + (3u << 16), r0, opptr(c, L.dYop, r0, d), d, true, L.pb2 + po * d));
+        c->kernels++;
+        EpiParams e1 = e;
+        e1.mode = EPI_ACT_BWD;
+        e1.act = TGP_ACT_GELU;
+        e1.zbuf = L.z[slot];
+        e1.ldz = H;
+        e1.op = opptr(c, L.dAop, r0, H);
+        e1.ld_op = H;
+        e1.colsum = L.pb + po * H;
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 10), d, H, H}, true, Opnd{L.dYop, c->max_batch, d, d},
+                         nullptr, false, H, M, d, r0, d, true, e1));
+        EpiParams es = e;
+        es.mode = EPI_STORE;
+        es.out0 = s.dh;
+        es.ld0 = d;
+        es.split_f = d;
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 8), H, d, d}, true, Opnd{L.dAop, c->max_batch, H, H},
+                         nullptr, false, d, M, H, r0, H, true, es));
+        // dx1 = g + LN2_bwd(dh2), kept in dx until the end of the layer
+        TGP_TRY(ln_bwd_any(c, s, pdl() && c->use_pdl, s.dh, L.x1[slot], L.mean2[slot], L.rstd2[slot], mparam(s, L, 6),
+                           g, dx, M, d, L.pg2 + po * d, L.pbt2 + po * d));
+        // attention branch: da = dx1 o keep2 -> bf16 operand (+ bo partial); dctx = da Wo
+        TGP_TRY(colwise(s.comp, pdl() && c->use_pdl, dx, d, nullptr, M, d, 0, th, dsc, c->seed, s.dstep,
+                        (uint32_t)l + (2u << 16), r0, opptr(c, L.dX1op, r0, d), d, true, L.po + po * d));
+        c->kernels++;
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 4), d, d, d}, true, Opnd{L.dX1op, c->max_batch, d, d},
+                         nullptr, false, d, M, d, r0, d, true, es));
+        TGP_TRY(attn_bwd(s.comp, opptr(c, L.QKVop, r0, d3), opptr(c, L.CTXop, r0, d), s.dh, L.lse[slot], s.attnD, M, d,
+                         L.L.n_heads, L.L.seq, r0, th, dsc, c->seed, s.dstep, (uint32_t)l + (1u << 16), s.tbuf));
+        c->kernels += 3;
+        TGP_TRY(colwise(s.comp, false, s.tbuf, d3, nullptr, M, d3, 0, 0u, 1.0f, c->seed, s.dstep, (uint32_t)l, r0,
+                        opptr(c, L.dQKVop, r0, d3), d3, true, L.pq + po * d3));
+        c->kernels++;
+        TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 2), d3, d, d}, true, Opnd{L.dQKVop, c->max_batch, d3, d3},
+                         nullptr, false, d, M, d3, r0, d3, true, es));
+        // dx = dx1 + LN1_bwd(dh1) (in place: each element read and written by the same thread)
+        TGP_TRY(ln_bwd_any(c, s, pdl() && c->use_pdl, s.dh, xin, L.mean[slot], L.rstd[slot], mparam(s, L, 0), dx, dx, M,
+                           d, L.pg + po * d, L.pbt + po * d));
+        dyop_ready = false;
+        break;
+      }
       case TGP_BATCHNORM: {
         TGP_TRY(bn_bwd(s.comp, g, xin, L.z[slot], L.bn_mu + pbn * din, L.bn_rstd + pbn * din, mparam(s, L, 0), M, din,
                        L.L.act, dx, L.pg + po * din, L.pb + po * din));
@@ -617,6 +791,33 @@ static int exec_wgrad(tgp_ctx* c, Stage& s, int B) {
         e.ldw = H;
         TGP_TRY(run_gemm(c, s, false, Opnd{L.dYop, B, dout, dout}, true, Opnd{L.Gop, B, H, H}, nullptr, true, dout, H, B,
                          0, B, false, e));
+        break;
+      }
+      case TGP_EMBED:
+        TGP_TRY(embed_wgrad(s.comp, s.self.fwd_in, s.d_in, B, L.dE, dout, L.L.vocab, L.L.seq, L.emb_scratch,
+                            gparam(s, L, 0), gparam(s, L, 1), acc));
+        c->kernels += 5;
+        break;
+      case TGP_LMHEAD:
+        e.dw = gparam(s, L, 2);
+        e.ldw = din;
+        TGP_TRY(run_gemm(c, s, false, Opnd{L.dYop, B, dout, dout}, true, Opnd{L.Hop, B, din, din}, nullptr, true, dout,
+                         din, B, 0, B, false, e));
+        break;
+      case TGP_TRANSFORMER: {
+        const int d = din, H = L.L.d_hidden, d3 = 3 * din;
+        struct {
+          int k;
+          void *a, *b;
+          int M, N;
+        } gw[4] = {{2, L.dQKVop, L.Hop, d3, d}, {4, L.dX1op, L.CTXop, d, d}, {8, L.dAop, L.H2op, H, d},
+                   {10, L.dYop, L.Gop, d, H}};
+        for (auto& q : gw) {
+          e.dw = gparam(s, L, q.k);
+          e.ldw = q.N;
+          TGP_TRY(run_gemm(c, s, false, Opnd{q.a, B, q.M, q.M}, true, Opnd{q.b, B, q.N, q.N}, nullptr, true, q.M, q.N,
+                           B, 0, B, false, e));
+        }
         break;
       }
       case TGP_BATCHNORM:
@@ -696,10 +897,12 @@ static void trace_end(tgp_ctx* c, Stage& s, cudaStream_t st, int stream_id, int 
 }
 
 static void micro_rows(const tgp_ctx* c, int B, int i, int* r0, int* M) {
-  const int q = B / c->m, r = B % c->m;
+  // split the B / unit samples (reading Z7), rows = samples x unit (unit = seq tokens for C5)
+  const int U = c->unit, S = B / U;
+  const int q = S / c->m, r = S % c->m;
   const int ii = i - 1;
-  *r0 = ii * q + std::min(ii, r);
-  *M = q + (ii < r ? 1 : 0);
+  *r0 = (ii * q + std::min(ii, r)) * U;
+  *M = (q + (ii < r ? 1 : 0)) * U;
 }
 
 // an event of stage s's device (reused every call; the waits bind at enqueue time)

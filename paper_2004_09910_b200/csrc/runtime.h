@@ -49,13 +49,20 @@ struct LayerRT {
   tgp_layer L{};
   int idx = 0, part = 0, d_skip = 0;
   int nparam = 0, pidx0 = 0;
-  int64_t poff[6] = {0}, pnum[6] = {0};
+  int64_t poff[12] = {0}, pnum[12] = {0};
   // deferred-dW operand stash (global rows, op dtype, max_batch rows)
   void *Xop = nullptr, *Zop = nullptr, *Hop = nullptr, *Gop = nullptr, *dAop = nullptr, *dYop = nullptr;
   // per-micro-batch column partials [m][w] fp32
   float *pb = nullptr, *pb2 = nullptr, *pg = nullptr, *pbt = nullptr;
   // per activation slot (checkpoint-managed): layer output, pre-activation, LN stats
   std::vector<float*> out, z, mean, rstd;
+  // GPT-2-shaped layers: block operand stash (global rows, bf16) -- QKV = [q|k|v] (attention input),
+  // CTX = attention output (Wo operand), H2 = LN2 output, dQKV / dX1 = gradients at the QKV / Wo GEMMs
+  void *QKVop = nullptr, *CTXop = nullptr, *H2op = nullptr, *dQKVop = nullptr, *dX1op = nullptr;
+  float *pq = nullptr, *po = nullptr, *pg2 = nullptr, *pbt2 = nullptr;  // column partials (bqkv, bo, LN2)
+  std::vector<float*> x1, mean2, rstd2, lse;  // per slot: attention-residual output, LN2 stats, log-sum-exp
+  float* dE = nullptr;        // embedding: [max_batch][d] fp32 output gradient (after the dropout mask)
+  int* emb_scratch = nullptr; // embedding: counting-sort scratch (3 vocab + max_batch ints)
   // BatchNorm per micro-batch statistics [m][d] and running stats [d]
   float *bn_mu = nullptr, *bn_var = nullptr, *bn_rstd = nullptr, *bn_rm = nullptr, *bn_rv = nullptr;
 };
@@ -95,6 +102,9 @@ struct Stage {
   float* partials = nullptr;  // all column-partial buffers of the partition (contiguous)
   size_t partial_floats = 0;
   float* gbuf[2] = {nullptr, nullptr};
+  float* tbuf = nullptr;   // [mb_cap][maxw] fp32 scratch (attention backward dqkv)
+  float* attnD = nullptr;  // [mb_cap][max heads] fp32 scratch (attention backward rowsum(dO o O))
+  double* ce_part = nullptr;  // [max_batch + 1] cross-entropy row losses (last partition)
   uint32_t* counters = nullptr;  // [8]
   double* loss_buf = nullptr;
   int* bn_rows = nullptr;
@@ -133,6 +143,7 @@ struct tgp_ctx {
   std::vector<tgp::Route> routes;
   std::vector<int> balance, devices, part_l0;
   int n = 0, m = 0, ckpt = 1, max_batch = 0, mb_cap = 0, nslots = 1;
+  int unit = 1;  // rows per sample (seq for the GPT-2-shaped kinds): micro-batches split samples
   int pb = 1;  // 16-row blocks per micro-batch: column-partial buffers are [m * pb][width]
   bool bf16 = false;
   uint64_t seed = 0;

@@ -13,7 +13,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TGP_LIB") or os.path.join(_HERE, "libtgp.so")
 
-KIND = {"linear": 0, "resmlp": 1, "merge": 2, "batchnorm": 3}
+KIND = {"linear": 0, "resmlp": 1, "merge": 2, "batchnorm": 3, "embed": 4, "transformer": 5, "lmhead": 6}
 ACT = {"none": 0, "relu": 1, "gelu": 2}
 CKPT = {"always": 0, "except_last": 1, "never": 2}
 DTYPE = {"fp32": 0, "bf16": 1}
@@ -28,7 +28,8 @@ class TgpError(RuntimeError):
 class Layer(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("d_in", ctypes.c_int32), ("d_out", ctypes.c_int32),
                 ("d_hidden", ctypes.c_int32), ("act", ctypes.c_int32), ("dropout", ctypes.c_float),
-                ("stash_route", ctypes.c_int32), ("pop_route", ctypes.c_int32)]
+                ("stash_route", ctypes.c_int32), ("pop_route", ctypes.c_int32), ("n_heads", ctypes.c_int32),
+                ("seq", ctypes.c_int32), ("vocab", ctypes.c_int32)]
 
 
 _lib = None
@@ -52,6 +53,7 @@ _SIGS = {
     "tgp_connect": [_P],
     "tgp_forward": [_P, _P, _I32, _P],
     "tgp_mse_loss_grad": [_P, _P, _P, _I32, _P, ctypes.POINTER(ctypes.c_double)],
+    "tgp_ce_loss_grad": [_P, _P, _P, _I32, _P, ctypes.POINTER(ctypes.c_double)],
     "tgp_backward": [_P, _P, _P],
     "tgp_step": [_P, ctypes.c_float],
     "tgp_num_params": [_P, ctypes.POINTER(_I32)],
@@ -161,7 +163,8 @@ def to_c_layers(layers):
     arr = (Layer * len(layers))()
     for q, L in enumerate(layers):
         arr[q] = Layer(KIND[L["kind"]], L["d_in"], L["d_out"], L.get("d_hidden", 0), ACT[L.get("act", "none")],
-                       float(L.get("dropout", 0.0)), L.get("stash", -1), L.get("pop", -1))
+                       float(L.get("dropout", 0.0)), L.get("stash", -1), L.get("pop", -1), L.get("n_heads", 0),
+                       L.get("seq", 0), L.get("vocab", 0))
     return arr
 
 
@@ -221,6 +224,14 @@ class Pipeline:
         _ready(y, t, dy)
         _check(lib().tgp_mse_loss_grad(self.h, _ptr(y), _ptr(t), B, _ptr(dy), ctypes.byref(loss)),
                "tgp_mse_loss_grad")
+        return loss.value
+
+    def ce_loss_grad(self, y, t, B, dy):
+        """Token cross-entropy (C5): y, dy [B, vocab] fp32, t [B] int32 on the last partition's device."""
+        loss = ctypes.c_double()
+        _ready(y, t, dy)
+        _check(lib().tgp_ce_loss_grad(self.h, _ptr(y), _ptr(t), B, _ptr(dy), ctypes.byref(loss)),
+               "tgp_ce_loss_grad")
         return loss.value
 
     def backward(self, dy, dx=None):

@@ -1,0 +1,81 @@
+"""GPU parity of the GPT-2-shaped stack (C5, BASELINE.json configs[4]; SURVEY 8(c) "pinned on shrunk
+C5"): embedding, pre-LN causal-attention blocks with dropout, LM head and token cross-entropy,
+pipelined through the C ABI, against the fp64 oracle on the same seeded tokens and parameters.
+Bar: normwise 2e-2 (bf16, reading Z15) on loss, logits, every gradient and every delta-theta;
+checkpoint modes bitwise equal (recompute under the restored Philox counters, reading Z17/Z21)."""
+import numpy as np
+import pytest
+
+from synth import configs as C
+
+from _gpu import compare, make_case, oracle_step
+
+pytestmark = pytest.mark.gpu
+
+
+def gpt_step(layers, params, x, t, *, m, n, ckpt, lr, balance=None, seed=0):
+    import torch
+
+    from paper_2004_09910_b200 import Pipeline
+
+    B = x.shape[0]
+    P = Pipeline(layers, chunks=m, devices=[0] * n, balance=balance, checkpoint=ckpt, max_batch=B, dtype="bf16",
+                 seed=seed)
+    for idx, p in enumerate(params):
+        P.set_param(idx, p)
+    dev = torch.device("cuda", 0)
+    X = torch.tensor(np.asarray(x, np.float32), device=dev)
+    T = torch.tensor(np.asarray(t, np.int32), device=dev)
+    V = layers[-1]["d_out"]
+    Y = torch.empty(B, V, device=dev)
+    DY = torch.empty(B, V, device=dev)
+    DX = torch.zeros(B, 1, device=dev)
+    P.forward(X, B, Y)
+    loss = P.ce_loss_grad(Y, T, B, DY)
+    P.backward(DY, DX)
+    rec = dict(loss=loss, y=Y.cpu().numpy().astype(np.float64), dx=np.zeros((B, 1)),
+               grads=[P.get_grad(i) for i in range(P.n_params)], log=P.issue_log(), kernels=P.kernel_count())
+    P.step(lr)
+    rec["params"] = [P.get_param(i) for i in range(P.n_params)]
+    P.close()
+    return rec
+
+
+def _run(layers, nseq, m, n, ckpt, balance=None, seed=11, lr=0.01):
+    x, t, params = make_case(layers, nseq, seed, "bf16")
+    ref = oracle_step(layers, params, x, t, lr=lr, m=m, seed=seed, step=0)
+    gpu = gpt_step(layers, params, x, t, m=m, n=n, ckpt=ckpt, lr=lr, balance=balance, seed=seed)
+    errs, bad = compare(gpu, ref, params, 2e-2, lr)
+    assert not bad, f"errors above 2e-2: {bad}"
+    return gpu, ref, errs
+
+
+def test_c5_small_parity_always():
+    cfg = C.C5_small()  # 4 blocks, d 128, 2 heads, seq 64, V 512, 8 seqs, m 4, n 2, dropout 0.1
+    gpu, ref, errs = _run(cfg.layers, cfg.batch, cfg.m, cfg.n, cfg.checkpoint, balance=[3, 3])
+    from oracle.schedule import records
+    assert np.array_equal(gpu["log"], records(cfg.m, cfg.n, cfg.checkpoint))
+
+
+def test_c5_no_dropout_single_partition():
+    layers = C.gpt2_stack(2, 128, 2, 64, 256, 0.0)
+    _run(layers, 2, 1, 1, "never")
+
+
+def test_c5_wider_multi_tile():
+    # d 256 (4 heads), seq 192 (3 attention tiles per sequence), MLP 1024, V 1024, 5 sequences split
+    # unevenly over m = 3 micro-batches ([2, 2, 1] sequences), n = 3
+    layers = C.gpt2_stack(3, 256, 4, 192, 1024, 0.1)
+    _run(layers, 5, 3, 3, "except_last", balance=[2, 1, 2])
+
+
+def test_c5_checkpoint_modes_bitwise():
+    layers = C.gpt2_stack(2, 128, 2, 128, 512, 0.1)
+    x, t, params = make_case(layers, 4, 3, "bf16")
+    outs = [gpt_step(layers, params, x, t, m=4, n=2, ckpt=mode, lr=0.01, balance=[2, 2], seed=3)
+            for mode in ("always", "except_last", "never")]
+    for o in outs[1:]:
+        assert o["loss"] == outs[0]["loss"]
+        assert np.array_equal(o["y"], outs[0]["y"])
+        for a, b in zip(o["grads"], outs[0]["grads"]):
+            assert np.array_equal(a, b)
