@@ -483,7 +483,7 @@ static int launch_tc(cudaStream_t st, bool pdl, const CUtensorMap& a, const CUte
     attr_done = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.M / 128, S, ntiles);
+  cfg.gridDim = dim3((p.M + 127) / 128, S, ntiles);
   cfg.blockDim = dim3(192, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
@@ -498,7 +498,7 @@ static int launch_tc(cudaStream_t st, bool pdl, const CUtensorMap& a, const CUte
   cfg.numAttrs = pdl ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b0, b1, dmap, p);
   if (e != cudaSuccess) {
-    set_error("gemm_tc launch (BN=%d A_MN=%d B_MN=%d grid=%d,%d,%d): %s", BN, (int)A_MN, (int)B_MN, p.M / 128, S,
+    set_error("gemm_tc launch (BN=%d A_MN=%d B_MN=%d grid=%d,%d,%d): %s", BN, (int)A_MN, (int)B_MN, (p.M + 127) / 128, S,
               ntiles, cudaGetErrorString(e));
     return -3;
   }
@@ -512,8 +512,9 @@ static int env_int(const char* name, int dflt) {
 
 int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B0, const TcMat* B1, bool b_mn,
             GemmParams p, int splits) {
-  if (p.M % 128 || p.K % 64 || p.M <= 0 || p.N <= 0) {
-    set_error("gemm_tc: unsupported shape M=%d N=%d K=%d (need M%%128==0, K%%64==0)", p.M, p.N, p.K);
+  if (p.M % 64 || p.K % 64 || p.M <= 0 || p.N <= 0) {
+    // M % 64: the last 128-row tile may be half empty (TMA zero-fills, the epilogue masks f >= M)
+    set_error("gemm_tc: unsupported shape M=%d N=%d K=%d (need M%%64==0, K%%64==0)", p.M, p.N, p.K);
     return -5;
   }
   const bool dw = p.epi.mode == EPI_DW;
@@ -531,7 +532,7 @@ int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B
   const int nkb = p.K / 64;
   int S = 1;
   if (!dw) {
-    const int mt = p.M / 128;
+    const int mt = (p.M + 127) / 128;
     S = splits > 0 ? splits : env_int("TGP_SPLITK", 0);
     if (S <= 0) {
       // ~one wave of 148 CTAs (measured: in the full step, split 4 beats split 8 at C2 although an

@@ -78,8 +78,10 @@ def umlp(d=2048, levels=4, blocks_per_level=2, mid_blocks=2, dropout=0.0):
     return L
 
 
-def gpt2_stack(n_layers=48, d=1600, n_heads=25, seq=1024, vocab=50257, dropout=0.1):
-    """C5 (configs[4]): embed + n_layers pre-LN GPT-2 blocks (MLP 4d, GELU) + final LN / LM head."""
+def gpt2_stack(n_layers=48, d=1600, n_heads=25, seq=1024, vocab=50304, dropout=0.1):
+    """C5 (configs[4]): embed + n_layers pre-LN GPT-2 blocks (MLP 4d, GELU) + final LN / LM head.
+    The GPT-2 vocabulary (50257) is padded to 50304 = 393 x 128 (whole tensor-core tiles for the LM
+    head; the padding rows are ordinary never-sampled tokens)."""
     L = [layer("embed", 1, d, dropout=dropout, seq=seq, vocab=vocab)]
     for _ in range(n_layers):
         L.append(layer("transformer", d, d, d_hidden=4 * d, act="gelu", dropout=dropout,
@@ -92,6 +94,12 @@ def C5_small(n=2, m=4, checkpoint="always", dropout=0.1, batch=8):
     """Shrunk C5 (SURVEY 8(c) pins): 4 blocks, d = 128, 2 heads, seq 64, V = 512, B = 8 seqs."""
     return Config("C5s", gpt2_stack(4, 128, 2, 64, 512, dropout), batch=batch, m=m, n=n,
                   checkpoint=checkpoint, dtype="bf16", lr=0.01)
+
+
+def C5(n=8, m=32, checkpoint="always", batch=32, n_layers=48):
+    """Full C5: 48 x (d 1600, 25 heads, seq 1024), V 50304, 32 sequences, m = 32 (1 seq each)."""
+    return Config("C5", gpt2_stack(n_layers), batch=batch, m=m, n=n, checkpoint=checkpoint, dtype="bf16",
+                  lr=0.01)
 
 
 def bn_mlp(n=4, d=256):

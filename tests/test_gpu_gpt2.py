@@ -79,3 +79,10 @@ def test_c5_checkpoint_modes_bitwise():
         assert np.array_equal(o["y"], outs[0]["y"])
         for a, b in zip(o["grads"], outs[0]["grads"]):
             assert np.array_equal(a, b)
+
+
+def test_c5_ragged_width():
+    # d = 320 (5 heads): 3d = 960 and d are not multiples of the 128-row tensor-core tile (full C5's
+    # d = 1600 is not either) and the LayerNorm takes the non-cluster path
+    layers = C.gpt2_stack(2, 320, 5, 64, 640, 0.1)
+    _run(layers, 3, 3, 2, "always", balance=[2, 2])
