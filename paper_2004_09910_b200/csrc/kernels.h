@@ -43,7 +43,7 @@ int gemm_simt(cudaStream_t st, bool pdl, SimtOperand A, SimtOperand B0, SimtOper
 int ln_fwd(cudaStream_t st, bool pdl, const float* x, int64_t ldx, int rows, int d, const float* gamma,
            const float* beta, void* h, int64_t ldh, bool h_bf16, float* mean, float* rstd);
 // LayerNorm backward: dx = dy + r (dn - mean(dn) - n mean(dn n)), dn = dh * gamma; writes the
-// per-micro-batch column partials dgamma_part = sum_rows dh n, dbeta_part = sum_rows dh.
+// column partials per 16-row block y (dgamma_part + y*d = sum_rows dh n, dbeta_part + y*d = sum_rows dh).
 int ln_bwd(cudaStream_t st, bool pdl, const float* dh, const float* x, const float* mean, const float* rstd,
            const float* gamma, const float* dy, float* dx, int rows, int d, float* dgamma_part, float* dbeta_part);
 // Cluster LayerNorm (features split over a cluster, row statistics exchanged through DSMEM in fixed

@@ -121,10 +121,62 @@ struct AttnArgs {
   uint32_t site;
 };
 
-TGP_DEV bool attn_keep(const AttnArgs& A, int s, int h, int q, int k) {
-  const uint64_t idx = (((uint64_t)(A.seq0 + s) * A.nh + h) * A.seq + q) * A.seq + k;
-  return dropout_keep(A.seed, *A.step, A.site, idx, A.thresh);
+// Keep bits of a 64-key tile for the accumulator layout (rows q0 and q0 + 8 of this thread, keys
+// kbase + nt*8 + 2t + {0, 1}): one Philox call yields the 4 words of 4 consecutive keys (the flat
+// index is a multiple of 4 at every 4-key group because seq % 64 == 0), so the two lanes t, t^1 that
+// share a group split the rows -- even t draws row q0, odd t row q0 + 8 -- and swap halves with one
+// shuffle: 8 Philox calls per thread per tile instead of 32.  Bit (nt*4 + c) = keep of element [nt][c].
+TGP_DEV uint32_t attn_keep_tile(const AttnArgs& A, int s, int h, int q0, int kbase) {
+  const int t = threadIdx.x & 3;
+  const int qm = q0 + (t & 1) * 8;
+  const uint64_t rowbase = (((uint64_t)(A.seq0 + s) * A.nh + h) * A.seq + qm) * A.seq;
+  const uint2 key = make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32));
+  const uint32_t step = *A.step;
+  uint32_t bits = 0;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) {
+    const uint64_t qi = (rowbase + kbase + nt * 8 + (t >> 1) * 4) >> 2;
+    const uint4 o = philox4x32_10(make_uint4((uint32_t)qi, (uint32_t)(qi >> 32), A.site, step), key);
+    const uint32_t mine = ((o.x >> 8) >= A.thresh ? 1u : 0u) | ((o.y >> 8) >= A.thresh ? 2u : 0u) |
+                          ((o.z >> 8) >= A.thresh ? 4u : 0u) | ((o.w >> 8) >= A.thresh ? 8u : 0u);
+    const uint32_t other = __shfl_xor_sync(0xffffffffu, mine, 1);
+    const uint32_t r0 = (t & 1) ? other : mine, r1 = (t & 1) ? mine : other;  // groups of rows q0, q0 + 8
+    const int off = (t & 1) * 2;  // this lane's keys 2t, 2t+1 inside the 4-key group
+    bits |= (((r0 >> off) & 3u) | (((r1 >> off) & 3u) << 2)) << (nt * 4);
+  }
+  return bits;
 }
+
+// Same for the transposed accumulator layout of the dK/dV kernel (rows = keys k0 + {0, 8} with
+// k0 = kbase + g, columns = queries qbase + nt*8 + 2t + {0, 1}).  The 4 consecutive keys of a Philox
+// group sit in the 4 lanes g = 4j..4j+3 (same t); lane j of the quartet draws the groups of
+// element c = j for every nt, then 4 shuffles hand every lane its own key's bit of each group.
+TGP_DEV uint32_t attn_keep_tile_t(const AttnArgs& A, int s, int h, int kbase_w, int qbase) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, j = g & 3;
+  const uint2 key = make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32));
+  const uint32_t step = *A.step;
+  const uint64_t hb = ((uint64_t)(A.seq0 + s) * A.nh + h) * A.seq;
+  const int kgrp = kbase_w + (g & ~3) + (j >> 1) * 8;  // key group of element c = j
+  uint32_t W = 0;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) {
+    const int q = qbase + nt * 8 + 2 * t + (j & 1);
+    const uint64_t qi = ((hb + q) * A.seq + kgrp) >> 2;
+    const uint4 o = philox4x32_10(make_uint4((uint32_t)qi, (uint32_t)(qi >> 32), A.site, step), key);
+    W |= (((o.x >> 8) >= A.thresh ? 1u : 0u) | ((o.y >> 8) >= A.thresh ? 2u : 0u) |
+          ((o.z >> 8) >= A.thresh ? 4u : 0u) | ((o.w >> 8) >= A.thresh ? 8u : 0u))
+         << (nt * 4);
+  }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int sl = 0; sl < 4; ++sl) {
+    const uint32_t V = __shfl_sync(0xffffffffu, W, (((g & ~3) + sl) << 2) | t);
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) bits |= ((V >> (nt * 4 + j)) & 1u) << (nt * 4 + sl);
+  }
+  return bits;
+}
+
 
 __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnArgs A, __nv_bfloat16* __restrict__ ctx, int64_t ldc,
                                                        float* __restrict__ lse) {
@@ -167,16 +219,14 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnArgs A, __nv_bfloat16
       m2[r] = mn;
       l[r] *= alpha[r];
     }
+    const uint32_t kb = A.thresh ? attn_keep_tile(A, s, h, q0, kt * TILE) : 0xFFFFFFFFu;
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float p = exp2f(sc[nt][c] - m2[c >> 1]);
         l[c >> 1] += p;
-        if (A.thresh) {
-          const int key = kt * TILE + nt * 8 + 2 * t + (c & 1), q = q0 + (c >> 1) * 8;
-          p = (key <= q && attn_keep(A, s, h, q, key)) ? p * A.dscale : 0.0f;
-        }
+        if (A.thresh) p = ((kb >> (nt * 4 + c)) & 1u) ? p * A.dscale : 0.0f;
         sc[nt][c] = p;
       }
 #pragma unroll
@@ -249,6 +299,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dkv_kernel(AttnArgs A, const flo
     mma_row_tile(p, ka, Qs);   // S^T[key][q]
     mma_row_tile(dp, va, Os);  // dP^T[key][q] = V dO^T
     float pd[8][4];
+    const uint32_t kb = A.thresh ? attn_keep_tile_t(A, s, h, kt * TILE + w * 16, qt * TILE) : 0xFFFFFFFFu;
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
@@ -258,7 +309,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dkv_kernel(AttnArgs A, const flo
         float dpv = dp[nt][c];
         float pdv = pr;
         if (A.thresh) {
-          const bool keep = key <= q && attn_keep(A, s, h, q, key);
+          const bool keep = (kb >> (nt * 4 + c)) & 1u;
           pdv = keep ? pr * A.dscale : 0.0f;
           dpv = keep ? dpv * A.dscale : 0.0f;
         }
@@ -311,6 +362,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(AttnArgs A, const floa
     float p[8][4] = {}, dp[8][4] = {};
     mma_row_tile(p, qa, Ks);   // S
     mma_row_tile(dp, oa, Vs);  // dP = dO V^T
+    const uint32_t kb = A.thresh ? attn_keep_tile(A, s, h, q0, kt * TILE) : 0xFFFFFFFFu;
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
@@ -318,7 +370,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(AttnArgs A, const floa
         const int key = kt * TILE + nt * 8 + 2 * t + (c & 1), q = q0 + (c >> 1) * 8;
         const float pr = key <= q ? exp2f(p[nt][c] * A.scale_log2 - ls[c >> 1]) : 0.0f;
         float dpv = dp[nt][c];
-        if (A.thresh) dpv = (key <= q && attn_keep(A, s, h, q, key)) ? dpv * A.dscale : 0.0f;
+        if (A.thresh) dpv = ((kb >> (nt * 4 + c)) & 1u) ? dpv * A.dscale : 0.0f;
         p[nt][c] = pr * (dpv - Dr[c >> 1]);  // dS
       }
     mma_p_tile(dq, p, Kt);  // dQ += dS K

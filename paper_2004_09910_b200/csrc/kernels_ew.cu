@@ -127,7 +127,8 @@ __global__ void ln_bwd_rows_kernel(const float* __restrict__ dh, const float* __
   }
 }
 
-// column partials over the micro-batch rows: dgamma = sum dh * n, dbeta = sum dh
+// column partials per 16-row block (same layout as the cluster LayerNorm and the GEMM colsum:
+// block y of the micro-batch writes dgp/dbp + y*d): dgamma = sum dh * n, dbeta = sum dh
 __global__ void ln_bwd_cols_kernel(const float* __restrict__ dh, const float* __restrict__ x,
                                    const float* __restrict__ mean, const float* __restrict__ rstd, int rows, int d,
                                    float* dgp, float* dbp) {
@@ -135,20 +136,21 @@ __global__ void ln_bwd_cols_kernel(const float* __restrict__ dh, const float* __
   griddep_launch();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= d) return;
+  const int r0 = blockIdx.y * 16, r1 = min(rows, r0 + 16);
   float sg = 0.0f, sb = 0.0f;
-  for (int r = 0; r < rows; ++r) {
+  for (int r = r0; r < r1; ++r) {
     const float v = dh[(int64_t)r * d + c];
     sg += v * ((x[(int64_t)r * d + c] - mean[r]) * rstd[r]);
     sb += v;
   }
-  dgp[c] = sg;
-  dbp[c] = sb;
+  dgp[(int64_t)blockIdx.y * d + c] = sg;
+  dbp[(int64_t)blockIdx.y * d + c] = sb;
 }
 
 int ln_bwd(cudaStream_t st, bool pdl, const float* dh, const float* x, const float* mean, const float* rstd,
            const float* gamma, const float* dy, float* dx, int rows, int d, float* dgp, float* dbp) {
-  int e = launch("ln_bwd_cols", ln_bwd_cols_kernel, dim3((d + 255) / 256), dim3(256), st, pdl, dh, x, mean, rstd,
-                 rows, d, dgp, dbp);
+  int e = launch("ln_bwd_cols", ln_bwd_cols_kernel, dim3((d + 127) / 128, (rows + 15) / 16), dim3(128), st, pdl, dh,
+                 x, mean, rstd, rows, d, dgp, dbp);
   if (e) return e;
   return launch("ln_bwd_rows", ln_bwd_rows_kernel, dim3(rows), dim3(d >= 1024 ? 256 : 128), st, pdl, dh, x, mean,
                 rstd, gamma, dy, dx, d);
