@@ -37,7 +37,10 @@ struct TcCfg {
   // Skinny (weight-streaming) tiles keep <= ~110 KB so two CTAs fit on an SM: with programmatic
   // dependent launch the NEXT GEMM's CTA becomes resident and streams its weights while this one
   // drains its epilogue.  Wide tiles (dW) take the whole SM.
-  static constexpr int BUDGET = BN <= 64 ? TGP_SKINNY_SMEM : 196608;
+  // BN = 128 tiles (the wide per-micro-batch GEMMs, N > 128 rows: C5's 1024-token micro-batches)
+  // also keep 3 stages (~97 KB) so two CTAs share an SM: one CTA's epilogue -- the instruction-bound
+  // part of these tiles (bias, GELU, fp32 z + bf16 operand stores) -- overlaps the other's mainloop.
+  static constexpr int BUDGET = BN <= 64 ? TGP_SKINNY_SMEM : BN == 128 ? 98304 : 196608;
   static constexpr int STAGES = (BUDGET / STAGE) > 12 ? 12 : (BUDGET / STAGE);
   static constexpr int RED_BYTES = 128 * BN * 4;           // fp32 partial tile (float4 quads)
   static constexpr int CS_BYTES = (BN / 4) * 128 * 4;      // column-sum partials [quad][feature]
@@ -526,7 +529,7 @@ int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B
       return -5;
     }
   } else {
-    BN = p.N <= 16 ? 16 : p.N <= 32 ? 32 : p.N <= 64 ? 64 : p.N <= 128 ? 128 : 256;
+    BN = p.N <= 16 ? 16 : p.N <= 32 ? 32 : p.N <= 64 ? 64 : 128;
   }
   const int ntiles = (p.N + BN - 1) / BN;
   const int nkb = p.K / 64;
