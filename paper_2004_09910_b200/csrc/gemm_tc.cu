@@ -406,32 +406,59 @@ __global__ void __launch_bounds__(192, 1)
     const bool want_cs = MODE == EPI_ACT_BWD && p.epi.colsum;
     if (et >= 0) {
       const uint32_t base = smem_u32(smem);
-      for (int it = et; it < rpr * nq; it += 128) {
-        const int fll = it & (rpr - 1), q = it >> lrpr;
-        const int fl = rank * rpr + fll;
-        const int f = m0 + fl;
-        const uint32_t off = (uint32_t)(((q >> 2) * 128 + fl) * 4 + ((q & 3) ^ (fl & 3))) * 16u;
-        float4 t[8];
+      // UNR work items per thread per round: their global epilogue operands (residual rows,
+      // saved pre-activations) are all requested before any is consumed, so the loads' latency
+      // overlaps (one item at a time left the epilogue waiting on each 4-element gather)
+      constexpr int UNR = 4;
+#pragma unroll 1
+      for (int it0 = et; it0 < rpr * nq; it0 += 128 * UNR) {
+        EpiPre pq[UNR][4];
+        float av[UNR][4];
 #pragma unroll
-        for (int s = 0; s < 8; ++s)
-          if (s < S) t[s] = ld_dsmem_f32x4(mapa_shared(base + off, (uint32_t)s));
-        float4 a = t[0];
+        for (int u = 0; u < UNR; ++u) {
+          const int it = it0 + 128 * u;
+          if (it >= rpr * nq) break;
+          const int fll = it & (rpr - 1), q = it >> lrpr;
+          const int fl = rank * rpr + fll;
+          const int f = m0 + fl;
+          const uint32_t off = (uint32_t)(((q >> 2) * 128 + fl) * 4 + ((q & 3) ^ (fl & 3))) * 16u;
+          float4 t[8];
 #pragma unroll
-        for (int s = 1; s < 8; ++s)
-          if (s < S) {
-            a.x += t[s].x;
-            a.y += t[s].y;
-            a.z += t[s].z;
-            a.w += t[s].w;
+          for (int s = 0; s < 8; ++s)
+            if (s < S) t[s] = ld_dsmem_f32x4(mapa_shared(base + off, (uint32_t)s));
+          float4 a = t[0];
+#pragma unroll
+          for (int s = 1; s < 8; ++s)
+            if (s < S) {
+              a.x += t[s].x;
+              a.y += t[s].y;
+              a.z += t[s].z;
+              a.w += t[s].w;
+            }
+          av[u][0] = a.x;
+          av[u][1] = a.y;
+          av[u][2] = a.z;
+          av[u][3] = a.w;
+          if (f < p.M) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (4 * q + e < nvalid) pq[u][e] = epi_load<MODE>(p.epi, f, nb + 4 * q + e);
           }
-        const float av[4] = {a.x, a.y, a.z, a.w};
-        float part = 0.0f;
-        if (f < p.M) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (4 * q + e < nvalid) part += epi_apply<MODE>(p.epi, f, nb + 4 * q + e, av[e]);
         }
-        if (want_cs) cs[q * rpr + fll] = part;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int it = it0 + 128 * u;
+          if (it >= rpr * nq) break;
+          const int fll = it & (rpr - 1), q = it >> lrpr;
+          const int f = m0 + rank * rpr + fll;
+          float part = 0.0f;
+          if (f < p.M) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (4 * q + e < nvalid) part += epi_finish<MODE>(p.epi, f, nb + 4 * q + e, av[u][e], pq[u][e]);
+          }
+          if (want_cs) cs[q * rpr + fll] = part;
+        }
       }
       if (want_cs) {
         asm volatile("bar.sync 1, 128;" ::: "memory");  // the 128 epilogue threads only

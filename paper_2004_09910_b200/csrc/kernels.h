@@ -24,6 +24,9 @@ struct TcMat {
 // operands stored [K][M] / [K][N], fp32 D; M, N multiples of 128.
 int gemm_dw(cudaStream_t st, const void* A, int64_t lda, const void* B, int64_t ldb, float* D, int64_t ldd, int M,
             int N, int K, bool accumulate);
+// Persistent tcgen05 GEMM for wide per-micro-batch GEMMs (gemm_wide.cu): same D = A B^T semantics and
+// epilogues as gemm_tc (B K-major, no second K-segment, no dW mode), one CTA per SM over 128 x 128 tiles.
+int gemm_wide(cudaStream_t st, const TcMat& A, bool a_mn, const TcMat& B, const GemmParams& p);
 int gemm_tc(cudaStream_t st, bool pdl, const TcMat& A, bool a_mn, const TcMat& B0, const TcMat* B1, bool b_mn,
             GemmParams p, int splits);
 // 2-D bf16 TMA descriptor over a row-major matrix, 128-byte swizzle, box {box_inner, box_outer}.

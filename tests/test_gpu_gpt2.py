@@ -13,7 +13,7 @@ from _gpu import compare, make_case, oracle_step
 pytestmark = pytest.mark.gpu
 
 
-def gpt_step(layers, params, x, t, *, m, n, ckpt, lr, balance=None, seed=0):
+def gpt_step(layers, params, x, t, *, m, n, ckpt, lr, balance=None, seed=0, options=None):
     import torch
 
     from paper_2004_09910_b200 import Pipeline
@@ -21,6 +21,8 @@ def gpt_step(layers, params, x, t, *, m, n, ckpt, lr, balance=None, seed=0):
     B = x.shape[0]
     P = Pipeline(layers, chunks=m, devices=[0] * n, balance=balance, checkpoint=ckpt, max_batch=B, dtype="bf16",
                  seed=seed)
+    for k, v in (options or {}).items():
+        P.set_option(k, v)
     for idx, p in enumerate(params):
         P.set_param(idx, p)
     dev = torch.device("cuda", 0)
@@ -86,3 +88,23 @@ def test_c5_ragged_width():
     # d = 1600 is not either) and the LayerNorm takes the non-cluster path
     layers = C.gpt2_stack(2, 320, 5, 64, 640, 0.1)
     _run(layers, 3, 3, 2, "always", balance=[2, 2])
+
+
+def test_c5_persistent_wide_gemm_matches_tile_gemm():
+    # micro-batches of 2 x 256 tokens: every per-micro-batch GEMM has N = 512 rows and takes the
+    # persistent gemm_wide kernel; compare with the one-tile-per-CTA gemm_tc (options off, no
+    # split-K) and with the oracle.  (Not bitwise: measured ~1e-6 relative differences between the
+    # two kernels' paths; both are deterministic run to run.)
+    layers = C.gpt2_stack(2, 256, 4, 256, 512, 0.1)
+    x, t, params = make_case(layers, 4, 5, "bf16")
+    a = gpt_step(layers, params, x, t, m=2, n=2, ckpt="except_last", lr=0.01, balance=[2, 2], seed=5)
+    a2 = gpt_step(layers, params, x, t, m=2, n=2, ckpt="except_last", lr=0.01, balance=[2, 2], seed=5)
+    b = gpt_step(layers, params, x, t, m=2, n=2, ckpt="except_last", lr=0.01, balance=[2, 2], seed=5,
+                 options={"gemm_wide": 0, "splitk": 1})
+    assert a["loss"] == a2["loss"] and all(np.array_equal(u, v) for u, v in zip(a["grads"], a2["grads"]))
+    assert abs(a["loss"] - b["loss"]) <= 1e-5 * abs(b["loss"])
+    for ga, gb in zip(a["grads"], b["grads"]):
+        assert np.max(np.abs(ga - gb)) <= 1e-3 * max(np.max(np.abs(gb)), 1e-12)
+    ref = oracle_step(layers, params, x, t, lr=0.01, m=2, seed=5, step=0)
+    errs, bad = compare(a, ref, params, 2e-2, 0.01)
+    assert not bad, bad
