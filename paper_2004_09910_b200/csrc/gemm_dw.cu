@@ -170,8 +170,10 @@ __global__ void __launch_bounds__(192, 1)
 // A: [K][M] bf16 (row stride lda elements), B: [K][N] bf16 (ldb), D: [M][N] fp32 (ldd).
 int gemm_dw(cudaStream_t st, const void* A, int64_t lda, const void* B, int64_t ldb, float* D, int64_t ldd, int M,
             int N, int K, bool accumulate) {
-  if (M % DW_BM || N % DW_BN || K <= 0) {
-    set_error("gemm_dw: unsupported shape M=%d N=%d K=%d (need M, N %% 128)", M, N, K);
+  if (M % 64 || N % 64 || K <= 0) {
+    // M, N % 64 (GPT-2's d = 1600): the last tile row / column is half empty -- TMA zero-fills the
+    // operand loads past M / N and clips the output stores
+    set_error("gemm_dw: unsupported shape M=%d N=%d K=%d (need M, N %% 64)", M, N, K);
     return -5;
   }
   const int Kp = (K + DW_BK - 1) / DW_BK * DW_BK;  // rows past K read as zeros (TMA bounds)
@@ -205,7 +207,8 @@ int gemm_dw(cudaStream_t st, const void* A, int64_t lda, const void* B, int64_t 
     }
     attr = true;
   }
-  DwParams p{M, N, Kp, N / DW_BN, (M / DW_BM) * (N / DW_BN), accumulate ? 1 : 0};
+  const int tn = (N + DW_BN - 1) / DW_BN, tm = (M + DW_BM - 1) / DW_BM;
+  DwParams p{M, N, Kp, tn, tm * tn, accumulate ? 1 : 0};
   const int grid = std::min(p.tiles, sms > 0 ? sms : 148);
   gemm_dw_kernel<<<grid, 192, DW_SMEM, st>>>(ma, mb, md, p);
   const cudaError_t e = cudaGetLastError();

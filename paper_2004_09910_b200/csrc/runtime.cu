@@ -180,7 +180,7 @@ static int run_gemm(tgp_ctx* c, Stage& s, bool pdl, Opnd A, bool a_mn, Opnd B0, 
       set_error("merge: d_in=%d must be a multiple of 64 in bf16 mode", k_seg);
       return TGP_E_UNSUPPORTED;
     }
-    if (e.mode == EPI_DW && a_mn && b_mn && !B1 && M % 128 == 0 && N % 128 == 0 && c->dw_persistent)
+    if (e.mode == EPI_DW && a_mn && b_mn && !B1 && M % 64 == 0 && N % 64 == 0 && c->dw_persistent)
       return gemm_dw(s.comp, A.p, A.ld, B0.p, B0.ld, e.dw, e.ldw, M, N, K, e.accumulate != 0);
     if (e.mode != EPI_DW && !B1 && !b_mn && N >= 256 && c->gemm_wide) return gemm_wide(s.comp, a, a_mn, b0, p);
     return gemm_tc(s.comp, pdl && c->use_pdl, a, a_mn, b0, B1 ? &b1 : nullptr, b_mn, p, c->splitk);
