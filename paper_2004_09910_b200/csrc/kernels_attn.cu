@@ -80,19 +80,33 @@ TGP_DEV void load_afrag(const __nv_bfloat16* S, int row0, uint32_t (*a)[4]) {
     a[kc][3] = ld32(S + (row0 + g + 8) * PITCH + kc * 16 + 8 + 2 * t);
   }
 }
-// acc[nt][4] (+)= A(16 x 64, fragments a) * B^T, B element (n, k) = Bs[n][k] for n < 64
-TGP_DEV void mma_row_tile(float (*acc)[4], const uint32_t (*a)[4], const __nv_bfloat16* Bs) {
-  const int g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
-#pragma unroll
-  for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-    for (int kc = 0; kc < 4; ++kc)
-      mma16816(acc[nt], a[kc], ld32(Bs + (nt * 8 + g) * PITCH + kc * 16 + 2 * t),
-               ld32(Bs + (nt * 8 + g) * PITCH + kc * 16 + 8 + 2 * t));
+TGP_DEV void ldsm_x4(uint32_t* r, const __nv_bfloat16* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
 }
-// acc[dt][4] += P(16 x 64 from accumulator layout p[nt][4]) * X, X element (k, n) = Xt[n][k]
-TGP_DEV void mma_p_tile(float (*acc)[4], const float (*p)[4], const __nv_bfloat16* Xt) {
-  const int g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
+TGP_DEV void ldsm_x4_t(uint32_t* r, const __nv_bfloat16* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+// acc[nt][4] (+)= A(16 x 64, fragments a) * B^T, B element (n, k) = Bs[n][k] for n < 64.  B fragments
+// by ldmatrix: matrix i of an x4 = 8 rows n x 8 columns k at k offset 8i (b0 / b1 of two k-chunks).
+TGP_DEV void mma_row_tile(float (*acc)[4], const uint32_t (*a)[4], const __nv_bfloat16* Bs) {
+  const int l = threadIdx.x & 31;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) {
+    uint32_t b[8];
+    ldsm_x4(b, Bs + (nt * 8 + (l & 7)) * PITCH + (l >> 3) * 8);
+    ldsm_x4(b + 4, Bs + (nt * 8 + (l & 7)) * PITCH + 32 + (l >> 3) * 8);
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) mma16816(acc[nt], a[kc], b[2 * kc], b[2 * kc + 1]);
+  }
+}
+// acc[dt][4] += P(16 x 64 keys, accumulator layout p[nt][4]) * X, X element (k, n) = Xs[k][n] (row-major
+// [64 k][64 n] tile): B fragments by ldmatrix.trans (matrix i: k rows 8(i&1).., n columns 8(i>>1)..).
+TGP_DEV void mma_p_tile(float (*acc)[4], const float (*p)[4], const __nv_bfloat16* Xs) {
+  const int l = threadIdx.x & 31;
 #pragma unroll
   for (int kc = 0; kc < 4; ++kc) {
     uint32_t a[4];
@@ -101,9 +115,12 @@ TGP_DEV void mma_p_tile(float (*acc)[4], const float (*p)[4], const __nv_bfloat1
     a[2] = pack2(p[2 * kc + 1][0], p[2 * kc + 1][1]);
     a[3] = pack2(p[2 * kc + 1][2], p[2 * kc + 1][3]);
 #pragma unroll
-    for (int dt = 0; dt < 8; ++dt)
-      mma16816(acc[dt], a, ld32(Xt + (dt * 8 + g) * PITCH + kc * 16 + 2 * t),
-               ld32(Xt + (dt * 8 + g) * PITCH + kc * 16 + 8 + 2 * t));
+    for (int dp = 0; dp < 4; ++dp) {
+      uint32_t b[4];
+      ldsm_x4_t(b, Xs + (kc * 16 + ((l >> 3) & 1) * 8 + (l & 7)) * PITCH + (2 * dp + (l >> 4)) * 8);
+      mma16816(acc[2 * dp], a, b[0], b[1]);
+      mma16816(acc[2 * dp + 1], a, b[2], b[3]);
+    }
   }
 }
 
@@ -180,7 +197,7 @@ TGP_DEV uint32_t attn_keep_tile_t(const AttnArgs& A, int s, int h, int kbase_w, 
 
 __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnArgs A, __nv_bfloat16* __restrict__ ctx, int64_t ldc,
                                                        float* __restrict__ lse) {
-  __shared__ __align__(16) __nv_bfloat16 Qs[TILE * PITCH], Ks[TILE * PITCH], Vt[TILE * PITCH];
+  __shared__ __align__(16) __nv_bfloat16 Qs[TILE * PITCH], Ks[TILE * PITCH], Vs[TILE * PITCH];
   const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, s = blockIdx.z;
   const int w = threadIdx.x >> 5, g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
   const int64_t base = (int64_t)s * A.seq;
@@ -194,7 +211,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnArgs A, __nv_bfloat16
   for (int kt = 0; kt <= qt; ++kt) {
     __syncthreads();
     load_tile(A.qkv + (base + kt * TILE) * A.ldq + A.d + h * HD, A.ldq, Ks, nullptr);
-    load_tile(A.qkv + (base + kt * TILE) * A.ldq + 2 * A.d + h * HD, A.ldq, nullptr, Vt);
+    load_tile(A.qkv + (base + kt * TILE) * A.ldq + 2 * A.d + h * HD, A.ldq, Vs, nullptr);
     __syncthreads();
     float sc[8][4] = {};
     mma_row_tile(sc, qa, Ks);
@@ -236,7 +253,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnArgs A, __nv_bfloat16
       o[dt][2] *= alpha[1];
       o[dt][3] *= alpha[1];
     }
-    mma_p_tile(o, sc, Vt);
+    mma_p_tile(o, sc, Vs);
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -272,7 +289,7 @@ __global__ void attn_bwd_prep_kernel(const float* __restrict__ dO, const __nv_bf
 __global__ void __launch_bounds__(128) attn_bwd_dkv_kernel(AttnArgs A, const float* __restrict__ dO, int64_t ldo,
                                                            const float* __restrict__ lse, const float* __restrict__ D,
                                                            float* __restrict__ dqkv, int64_t ldg) {
-  __shared__ __align__(16) __nv_bfloat16 Qs[TILE * PITCH], Qt[TILE * PITCH], Os[TILE * PITCH], Ot[TILE * PITCH];
+  __shared__ __align__(16) __nv_bfloat16 Qs[TILE * PITCH], Os[TILE * PITCH];
   __shared__ float ls[TILE], Ds[TILE];
   const int kt = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
   const int w = threadIdx.x >> 5, g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
@@ -288,8 +305,8 @@ __global__ void __launch_bounds__(128) attn_bwd_dkv_kernel(AttnArgs A, const flo
   const int k0 = kt * TILE + w * 16 + g;
   for (int qt = kt; qt < nq; ++qt) {
     __syncthreads();
-    load_tile(A.qkv + (base + qt * TILE) * A.ldq + h * HD, A.ldq, Qs, Qt);
-    load_tile_f32(dO + (base + qt * TILE) * ldo + h * HD, ldo, Os, Ot);
+    load_tile(A.qkv + (base + qt * TILE) * A.ldq + h * HD, A.ldq, Qs, nullptr);
+    load_tile_f32(dO + (base + qt * TILE) * ldo + h * HD, ldo, Os, nullptr);
     if (threadIdx.x < TILE) {
       ls[threadIdx.x] = lse[(base + qt * TILE + threadIdx.x) * A.nh + h];
       Ds[threadIdx.x] = D[(base + qt * TILE + threadIdx.x) * A.nh + h];
@@ -316,8 +333,8 @@ __global__ void __launch_bounds__(128) attn_bwd_dkv_kernel(AttnArgs A, const flo
         pd[nt][c] = pdv;
         p[nt][c] = pr * (dpv - Ds[ql]);  // dS^T
       }
-    mma_p_tile(dv, pd, Ot);  // dV += Pd^T dO
-    mma_p_tile(dk, p, Qt);   // dK += dS^T Q
+    mma_p_tile(dv, pd, Os);  // dV += Pd^T dO
+    mma_p_tile(dk, p, Qs);   // dK += dS^T Q
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -336,7 +353,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dkv_kernel(AttnArgs A, const flo
 __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(AttnArgs A, const float* __restrict__ dO, int64_t ldo,
                                                           const float* __restrict__ lse, const float* __restrict__ D,
                                                           float* __restrict__ dqkv, int64_t ldg) {
-  __shared__ __align__(16) __nv_bfloat16 Ks[TILE * PITCH], Kt[TILE * PITCH], Vs[TILE * PITCH];
+  __shared__ __align__(16) __nv_bfloat16 Ks[TILE * PITCH], Vs[TILE * PITCH];
   const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, s = blockIdx.z;
   const int w = threadIdx.x >> 5, g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
   const int64_t base = (int64_t)s * A.seq;
@@ -356,7 +373,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(AttnArgs A, const floa
   float dq[8][4] = {};
   for (int kt = 0; kt <= qt; ++kt) {
     __syncthreads();
-    load_tile(A.qkv + (base + kt * TILE) * A.ldq + A.d + h * HD, A.ldq, Ks, Kt);
+    load_tile(A.qkv + (base + kt * TILE) * A.ldq + A.d + h * HD, A.ldq, Ks, nullptr);
     load_tile(A.qkv + (base + kt * TILE) * A.ldq + 2 * A.d + h * HD, A.ldq, Vs, nullptr);
     __syncthreads();
     float p[8][4] = {}, dp[8][4] = {};
@@ -373,7 +390,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(AttnArgs A, const floa
         if (A.thresh) dpv = ((kb >> (nt * 4 + c)) & 1u) ? dpv * A.dscale : 0.0f;
         p[nt][c] = pr * (dpv - Dr[c >> 1]);  // dS
       }
-    mma_p_tile(dq, p, Kt);  // dQ += dS K
+    mma_p_tile(dq, p, Ks);  // dQ += dS K
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
