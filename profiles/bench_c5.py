@@ -31,9 +31,10 @@ ap.add_argument("--parts", type=int, default=1)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--checkpoint", default="always")
+ap.add_argument("--dropout", type=float, default=0.1)
 a = ap.parse_args()
 
-layers = C.gpt2_stack(a.layers)
+layers = C.gpt2_stack(a.layers, dropout=a.dropout)
 seq, V, d = layers[1]["seq"], layers[-1]["d_out"], layers[1]["d_in"]
 T = a.seqs * seq
 free0 = torch.cuda.mem_get_info(0)[0]
@@ -73,7 +74,7 @@ attn = sum(2 * seq * d for L in layers if L["kind"] == "transformer")
 fwd = 2 * n_mm + attn
 mult = 4 if a.checkpoint == "always" else 3
 flops = fwd * mult * T
-out = dict(workload=f"C5: embed + {a.layers} x GPT-2 block (d {d}, 25 heads, seq {seq}, dropout 0.1) + LM head V {V}",
+out = dict(workload=f"C5: embed + {a.layers} x GPT-2 block (d {d}, 25 heads, seq {seq}, dropout {a.dropout}) + LM head V {V}",
            seqs=a.seqs, chunks=a.chunks, parts_on_one_gpu=a.parts, checkpoint=a.checkpoint,
            ms_per_step=ms, seq_per_s=a.seqs / ms * 1e3, tokens_per_s=T / ms * 1e3,
            model_tflops=flops / ms * 1e-9, algorithmic_flop_per_step=flops,
