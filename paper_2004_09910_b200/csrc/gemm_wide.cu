@@ -9,7 +9,7 @@
 // it (ncu: tensor pipe ~2 % active, profiles/r4b_c5_gemm_*).  Here one CTA per SM loops over 128 x 128
 // tiles (static round-robin, n fastest so the CTAs working on one weight tile run together and share
 // it through L2) with the accumulator double-buffered in TMEM: tile t+1's TMA loads and MMAs run
-// while the eight epilogue warps finish tile t straight from TMEM (thread = feature, 32 rows per
+// while the sixteen epilogue warps finish tile t straight from TMEM (thread = feature, 32 rows per
 // tcgen05.ld chunk; every global operand of a chunk is requested before any is used).
 // Deterministic: each output element comes from one CTA with a fixed k order (no split-K), so F'
 // reproduces F bit-exactly (reading Z21).
@@ -29,9 +29,13 @@ constexpr int WG_STAGES = 6;
 constexpr int WG_OFF_BAR = WG_STAGES * WG_STAGE;
 constexpr int WG_SMEM = WG_OFF_BAR + 256 + 1024;
 // The epilogue, not the MMA, bounds these tiles (~40 instructions per element vs 5.5 us of tensor
-// work per 128 x 128 x 1600 tile), so 8 epilogue warps: two per TMEM lane quadrant, each taking
-// half of the tile's 32-row chunks.
-constexpr int WG_EPI_WARPS = 8;
+// work per 128 x 128 x 1600 tile), so 16 epilogue warps: four per TMEM lane quadrant, each taking
+// one of the tile's four 32-row chunks (measured C5 8-layer step: 4 warps 83 ms, 8 warps 69 ms,
+// 16 warps 62 ms).
+#ifndef TGP_WG_EPI_WARPS
+#define TGP_WG_EPI_WARPS 16
+#endif
+constexpr int WG_EPI_WARPS = TGP_WG_EPI_WARPS;
 constexpr int WG_THREADS = 64 + 32 * WG_EPI_WARPS;
 
 struct WideParams {
@@ -139,38 +143,30 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
       mbar_wait(&tfull[buf], (uint32_t)(u & 1));
       tc_fence_after();
       const uint32_t taddr = tmem + (uint32_t)(buf * WG_BN) + ((uint32_t)(lg * 32) << 16);
+      // 8-column groups (tcgen05.ld 32x32b.x8): 8 operand gathers in flight per thread, and a loop
+      // body small enough for the instruction cache (the fully unrolled 32-column body stalled on
+      // instruction fetch, ncu "no_instructions")
+      float part = 0.0f;
 #pragma unroll 1
-      for (int c = c0; c < c0 + CPW; ++c) {
-        const int r0 = nb + c * 32;
-        float v[32];
-        tmem_ld16(taddr + c * 32, v);
-        tmem_ld16(taddr + c * 32 + 16, v + 16);
-        if (c == c0 + CPW - 1) {  // this warp's part of the accumulator is in registers
+      for (int cg = c0 * 4; cg < (c0 + CPW) * 4; ++cg) {
+        const int r0 = nb + cg * 8;
+        float v[8];
+        tmem_ld8(taddr + cg * 8, v);
+        if (cg == (c0 + CPW) * 4 - 1) {  // this warp's part of the accumulator is in registers
           tc_fence_before();
           mbar_arrive(&tempty[buf]);
         }
-        if (r0 >= p.N) continue;
-        EpiPre pre[32];
-        if (fok) {
+        if (r0 >= p.N || !fok) continue;
+        EpiPre pre[8];
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (r0 + j < p.N) pre[j] = epi_load<MODE>(p.epi, f, r0 + j);
-        }
-        float part0 = 0.0f, part1 = 0.0f;
-        if (fok) {
+        for (int j = 0; j < 8; ++j)
+          if (r0 + j < p.N) pre[j] = epi_load<MODE>(p.epi, f, r0 + j);
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (r0 + j < p.N) {
-              const float q = epi_finish<MODE>(p.epi, f, r0 + j, nkb ? v[j] : 0.0f, pre[j]);
-              if (j < 16)
-                part0 += q;
-              else
-                part1 += q;
-            }
-        }
-        if (MODE == EPI_ACT_BWD && p.epi.colsum && fok) {  // per-16-row column partials (fixed order)
-          p.epi.colsum[(int64_t)(r0 / 16) * p.M + f] = part0;
-          if (r0 + 16 < p.N) p.epi.colsum[(int64_t)(r0 / 16 + 1) * p.M + f] = part1;
+        for (int j = 0; j < 8; ++j)
+          if (r0 + j < p.N) part += epi_finish<MODE>(p.epi, f, r0 + j, nkb ? v[j] : 0.0f, pre[j]);
+        if (MODE == EPI_ACT_BWD && ((cg & 1) || r0 + 8 >= p.N)) {  // per-16-row column partials
+          if (p.epi.colsum) p.epi.colsum[(int64_t)(r0 / 16) * p.M + f] = part;
+          part = 0.0f;
         }
       }
     }
