@@ -18,9 +18,12 @@
 namespace tgp {
 
 namespace {
-constexpr int DW_BM = 128, DW_BN = 128, DW_BK = 64;
+#ifndef TGP_DW_BN
+#define TGP_DW_BN 128
+#endif
+constexpr int DW_BM = 128, DW_BN = TGP_DW_BN, DW_BK = 64;
 constexpr int DW_STAGE = (DW_BM + DW_BN) * DW_BK * 2;  // 32 KB
-constexpr int DW_STAGES = 5;
+constexpr int DW_STAGES = DW_BN == 256 ? 4 : 5;
 constexpr int DW_CHUNK = 128 * 32 * 4;                 // 16 KB epilogue chunk (128 rows x 32 fp32)
 constexpr int DW_OFF_C = DW_STAGES * DW_STAGE;
 constexpr int DW_OFF_BAR = DW_OFF_C + 2 * DW_CHUNK;
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 256);
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * DW_BN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -92,8 +95,8 @@ __global__ void __launch_bounds__(192, 1)
           const int k = kb * DW_BK;
           tma_load_2d(&tmA, &full[s], st, m0, k, pol);
           tma_load_2d(&tmA, &full[s], st + 8192, m0 + 64, k, pol);
-          tma_load_2d(&tmB, &full[s], st + 16384, n0, k, pol);
-          tma_load_2d(&tmB, &full[s], st + 16384 + 8192, n0 + 64, k, pol);
+#pragma unroll
+          for (int c = 0; c < DW_BN / 64; ++c) tma_load_2d(&tmB, &full[s], st + 16384 + c * 8192, n0 + c * 64, k, pol);
         }
       }
     }
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(192, 1)
     if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 256);
+  if (warp == 1) tmem_dealloc(tmem, 2 * DW_BN);
 }
 
 // A: [K][M] bf16 (row stride lda elements), B: [K][N] bf16 (ldb), D: [M][N] fp32 (ldd).
