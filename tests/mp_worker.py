@@ -30,12 +30,17 @@ def main():
     if cfg == "umlp":
         layers = C.umlp(d=256, levels=2, blocks_per_level=1, mid_blocks=1)
         bal = None
+    elif cfg == "gpt2":
+        layers = C.gpt2_stack(3, 128, 2, 64, 512, 0.1)  # embed + 3 blocks + LM head
+        bal = {2: [2, 3], 3: [2, 2, 1]}[ws]
     else:
         # "stream": d = 512, eligible for the persistent stream kernel in every partition
         layers = C.resmlp_stack(2 * ws, 512 if cfg == "stream" else 256, dropout=0.1)
         bal = [2] * ws
     B, m, lr, seed = (64 if cfg == "stream" else 32), 4, 0.05, 11
-    x, t = G.inputs(layers, B, seed=seed, dtype="bf16")
+    x, t = G.inputs(layers, 4 if cfg == "gpt2" else B, seed=seed, dtype="bf16")
+    if cfg == "gpt2":
+        B, m = x.shape[0], 2  # 4 sequences of 64 tokens, 2 micro-batches
     params = G.params(layers, seed=seed, dtype="bf16")
     devices = [-1] * ws
     devices[rank] = dev
@@ -50,6 +55,7 @@ def main():
     first, last = rank == 0, rank == ws - 1
     X = torch.tensor(x, device="cuda") if first else None
     T = torch.tensor(t, device="cuda") if last else None
+    lossf = P.ce_loss_grad if cfg == "gpt2" else P.mse_loss_grad
     Y = torch.empty(B, layers[-1]["d_out"], device="cuda") if last else None
     DY = torch.empty_like(Y) if last else None
     DX = torch.empty(B, layers[0]["d_in"], device="cuda") if first else None
@@ -57,7 +63,7 @@ def main():
     for step in range(2):
         P.forward(X, B, Y)
         if last:
-            res[f"loss{step}"] = np.array(P.mse_loss_grad(Y, T, B, DY))
+            res[f"loss{step}"] = np.array(lossf(Y, T, B, DY))
             res[f"y{step}"] = Y.cpu().numpy()
         P.backward(DY, DX)
         if first:
