@@ -23,6 +23,9 @@ namespace tgp {
 
 namespace {
 
+#ifndef TGP_ATTN_MINB
+#define TGP_ATTN_MINB 1
+#endif
 constexpr int HD = 64;     // head dim
 constexpr int TILE = 64;   // query / key tile
 constexpr int PITCH = 72;  // smem row pitch (bf16 elements): conflict-free fragment loads
@@ -195,7 +198,7 @@ TGP_DEV uint32_t attn_keep_tile_t(const AttnArgs& A, int s, int h, int kbase_w, 
 }
 
 
-__global__ void __launch_bounds__(128) attn_fwd_kernel(AttnArgs A, __nv_bfloat16* __restrict__ ctx, int64_t ldc,
+__global__ void __launch_bounds__(128, TGP_ATTN_MINB) attn_fwd_kernel(AttnArgs A, __nv_bfloat16* __restrict__ ctx, int64_t ldc,
                                                        float* __restrict__ lse) {
   __shared__ __align__(16) __nv_bfloat16 Qs[TILE * PITCH], Ks[TILE * PITCH], Vs[TILE * PITCH];
   const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, s = blockIdx.z;
@@ -286,7 +289,7 @@ __global__ void attn_bwd_prep_kernel(const float* __restrict__ dO, const __nv_bf
 }
 
 // dK, dV of one key tile: loop over the query tiles at or after it.
-__global__ void __launch_bounds__(128) attn_bwd_dkv_kernel(AttnArgs A, const float* __restrict__ dO, int64_t ldo,
+__global__ void __launch_bounds__(128, TGP_ATTN_MINB) attn_bwd_dkv_kernel(AttnArgs A, const float* __restrict__ dO, int64_t ldo,
                                                            const float* __restrict__ lse, const float* __restrict__ D,
                                                            float* __restrict__ dqkv, int64_t ldg) {
   __shared__ __align__(16) __nv_bfloat16 Qs[TILE * PITCH], Os[TILE * PITCH];
@@ -350,7 +353,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dkv_kernel(AttnArgs A, const flo
 }
 
 // dQ of one query tile: loop over the key tiles at or before it.
-__global__ void __launch_bounds__(128) attn_bwd_dq_kernel(AttnArgs A, const float* __restrict__ dO, int64_t ldo,
+__global__ void __launch_bounds__(128, TGP_ATTN_MINB) attn_bwd_dq_kernel(AttnArgs A, const float* __restrict__ dO, int64_t ldo,
                                                           const float* __restrict__ lse, const float* __restrict__ D,
                                                           float* __restrict__ dqkv, int64_t ldg) {
   __shared__ __align__(16) __nv_bfloat16 Ks[TILE * PITCH], Vs[TILE * PITCH];
