@@ -25,7 +25,9 @@ struct EpiPre {
   bool keep = true;
 };
 
-template <int MODE>
+// WITH_KEEP = false: the caller supplies EpiPre::keep itself (gemm_wide draws the dropout bits of
+// 4 features x 4 rows per Philox call and shares them across lanes)
+template <int MODE, bool WITH_KEEP = true>
 TGP_DEV EpiPre epi_load(const EpiParams& e, int f, int r) {
   EpiPre q;
   if constexpr (MODE == EPI_LINEAR_FWD) {
@@ -36,7 +38,7 @@ TGP_DEV EpiPre epi_load(const EpiParams& e, int f, int r) {
   } else if constexpr (MODE == EPI_ACT_BWD) {
     if (e.act) q.a = e.zbuf[(int64_t)r * e.ldz + f];
   }
-  if constexpr (MODE == EPI_LINEAR_FWD || MODE == EPI_ACT_BWD || MODE == EPI_RESID_FWD) {
+  if constexpr (WITH_KEEP && (MODE == EPI_LINEAR_FWD || MODE == EPI_ACT_BWD || MODE == EPI_RESID_FWD)) {
     if (e.drop_thresh) {
       const uint64_t idx = (uint64_t)(e.row_global0 + r) * (uint64_t)e.drop_width + (uint64_t)f;
       q.keep = dropout_keep(e.seed, *e.step, e.site, idx, e.drop_thresh);

@@ -147,6 +147,11 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
       // body small enough for the instruction cache (the fully unrolled 32-column body stalled on
       // instruction fetch, ncu "no_instructions")
       float part = 0.0f;
+      // shared dropout draws (needs the 4-feature groups aligned: width % 4 == 0; the ACT_BWD
+      // epilogue keeps the per-element draw)
+      const bool wide_drop = (MODE == EPI_LINEAR_FWD || MODE == EPI_RESID_FWD) && p.epi.drop_thresh &&
+                             (p.epi.drop_width & 3) == 0;
+      const uint32_t dstep = wide_drop ? *p.epi.step : 0u;
 #pragma unroll 1
       for (int cg = c0 * 4; cg < (c0 + CPW) * 4; ++cg) {
         const int r0 = nb + cg * 8;
@@ -156,11 +161,41 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
           tc_fence_before();
           mbar_arrive(&tempty[buf]);
         }
-        if (r0 >= p.N || !fok) continue;
+        if (r0 >= p.N) continue;
+        // dropout bits of rows r0..r0+7 at this thread's feature: the flat index (row * width + f)
+        // of 4 consecutive features is one Philox call (width % 4 == 0), so lane (lane & ~3) + k
+        // draws row r0 + 4h + k for the 4 features of its group and 4 shuffles per half hand every
+        // lane its own bit -- 2 calls per thread per 8 rows instead of 8 (same decisions, O8)
+        uint32_t kbits = 0xFFu;
+        if (wide_drop) {
+          kbits = 0u;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint64_t rg = (uint64_t)(p.epi.row_global0 + r0 + hh * 4 + (lane & 3));
+            const uint64_t qi = (rg * (uint64_t)p.epi.drop_width + (uint64_t)(f & ~3)) >> 2;
+            const uint4 o = philox4x32_10(make_uint4((uint32_t)qi, (uint32_t)(qi >> 32), p.epi.site, dstep),
+                                          make_uint2((uint32_t)p.epi.seed, (uint32_t)(p.epi.seed >> 32)));
+            const uint32_t wbits = ((o.x >> 8) >= p.epi.drop_thresh ? 1u : 0u) | ((o.y >> 8) >= p.epi.drop_thresh ? 2u : 0u) |
+                                   ((o.z >> 8) >= p.epi.drop_thresh ? 4u : 0u) | ((o.w >> 8) >= p.epi.drop_thresh ? 8u : 0u);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t b = __shfl_sync(0xffffffffu, wbits, (lane & ~3) | k);
+              kbits |= ((b >> (lane & 3)) & 1u) << (hh * 4 + k);
+            }
+          }
+        }
+        if (!fok) continue;
         EpiPre pre[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (r0 + j < p.N) pre[j] = epi_load<MODE>(p.epi, f, r0 + j);
+          if (r0 + j < p.N) {
+            if (wide_drop) {
+              pre[j] = epi_load<MODE, false>(p.epi, f, r0 + j);
+              pre[j].keep = (kbits >> j) & 1u;
+            } else {
+              pre[j] = epi_load<MODE>(p.epi, f, r0 + j);
+            }
+          }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           if (r0 + j < p.N) part += epi_finish<MODE>(p.epi, f, r0 + j, nkb ? v[j] : 0.0f, pre[j]);
