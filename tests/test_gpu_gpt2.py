@@ -108,3 +108,11 @@ def test_c5_persistent_wide_gemm_matches_tile_gemm():
     ref = oracle_step(layers, params, x, t, lr=0.01, m=2, seed=5, step=0)
     errs, bad = compare(a, ref, params, 2e-2, 0.01)
     assert not bad, bad
+
+
+def test_c5_full_width_parity():
+    # the full C5 layer shapes (d 1600 = 25 heads x 64, MLP 6400, seq 1024, V 50304; ragged 128-row
+    # tiles, 16 attention tiles per sequence, 1024-row micro-batches on the persistent GEMM) on a
+    # shortened stack: embed + 2 blocks + LM head, 2 sequences, m = 2, n = 2, dropout 0.1, always
+    layers = C.gpt2_stack(2, 1600, 25, 1024, 50304, 0.1)
+    _run(layers, 2, 2, 2, "always", balance=[2, 2], seed=21)
