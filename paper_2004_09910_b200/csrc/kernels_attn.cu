@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "host.h"
@@ -273,6 +274,195 @@ __global__ void __launch_bounds__(128, TGP_ATTN_MINB) attn_fwd_kernel(AttnArgs A
           pack2(o[dt][2 * r] * inv, o[dt][2 * r + 1] * inv);
     if (t == 0) lse[row * A.nh + h] = m2[r] + log2f(l[r]);  // log2 domain
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// tcgen05 forward (seq % 128 == 0): one CTA of 4 warps per (128-query tile, head, sequence); thread
+// = query row = TMEM lane, so the softmax statistics of a row are thread-local.  Per 128-key tile:
+// S = Q K^T (tcgen05.mma 128x128x64, fp32 in TMEM) -> registers -> mask, online softmax, Philox
+// dropout -> P (bf16) into a 128-byte-swizzled K-major smem tile -> O_tile = P V (tcgen05.mma
+// 128x64x128, V read MN-major) -> registers, O = alpha O + O_tile.  K / V tiles double-buffered with
+// cp.async into the swizzled layout; Q, K and P are K-major operands, V an MN-major one.  Same
+// arithmetic as the mma.sync kernel up to accumulation order (both sides bf16 operands, fp32 sums).
+TGP_DEV void cp_async16(void* smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+TGP_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+TGP_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int TCQ = 128;
+constexpr int TC_SMEM = 16384 * 7 + 64 + 1024 + 1024;  // Q, K[2], V[2], P (2 chunks), barriers, row exchange + align
+
+// row r, 16-byte chunk c of a [rows][64] bf16 tile in the SW128 layout
+TGP_DEV uint32_t sw_off(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+TGP_DEV void load_sw_tile(const __nv_bfloat16* g, int64_t ld, uint8_t* S) {
+  for (int q = threadIdx.x; q < TCQ * 8; q += blockDim.x) {
+    const int r = q >> 3, c = q & 7;
+    cp_async16(S + sw_off(r, c), g + (int64_t)r * ld + c * 8);
+  }
+}
+
+#ifndef TGP_ATTN_TC_MINB
+#define TGP_ATTN_TC_MINB 1
+#endif
+__global__ void __launch_bounds__(256, TGP_ATTN_TC_MINB) attn_fwd_tc_kernel(AttnArgs A, __nv_bfloat16* __restrict__ ctx, int64_t ldc,
+                                                          float* __restrict__ lse) {
+  // 8 warps: warp w reads TMEM lane quadrant (w & 3) and owns key half / output-column half (w >> 2)
+  // of its rows, so two threads share a query row (row max and sum combined through smem)
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Qs = sm;
+  uint8_t* Ks0 = sm + 16384;
+  uint8_t* Vs0 = sm + 3 * 16384;
+  uint8_t* Ps = sm + 5 * 16384;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 7 * 16384);  // [0] S done, [1] PV done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  float* xch = reinterpret_cast<float*>(sm + 7 * 16384 + 64);  // [2][128] row max / sum halves
+  const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int hf = w >> 2, row = (w & 3) * 32 + lane;
+  const int64_t base = (int64_t)s * A.seq;
+  const int q = qt * TCQ + row;
+  const __nv_bfloat16* Kg = A.qkv + base * A.ldq + A.d + h * HD;
+  const __nv_bfloat16* Vg = A.qkv + base * A.ldq + 2 * A.d + h * HD;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  if (w == 0) tmem_alloc(tslot, 256);
+  load_sw_tile(A.qkv + (base + qt * TCQ) * A.ldq + h * HD, A.ldq, Qs);
+  load_sw_tile(Kg, A.ldq, Ks0);
+  load_sw_tile(Vg, A.ldq, Vs0);
+  cp_async_commit();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tS = tmem, tO = tmem + 128;
+  const uint32_t lane_off = (uint32_t)((w & 3) * 32) << 16;
+  constexpr uint32_t idS = make_idesc_bf16(128, 128, false, false);
+  constexpr uint32_t idO = make_idesc_bf16(128, 64, false, true);
+  const uint64_t rowbase = (((uint64_t)(A.seq0 + s) * A.nh + h) * A.seq + q) * A.seq;
+  const uint2 pkey = make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32));
+  const uint32_t pstep = A.thresh ? *A.step : 0u;
+  float m2 = -INFINITY, l = 0.0f;
+  float o[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) o[i] = 0.0f;
+  const int nkt = qt + 1;
+  for (int kt = 0; kt < nkt; ++kt) {
+    const int st = kt & 1;
+    uint8_t* Ks = Ks0 + st * 16384;
+    uint8_t* Vs = Vs0 + st * 16384;
+    if (kt + 1 < nkt) {
+      load_sw_tile(Kg + (int64_t)(kt + 1) * TCQ * A.ldq, A.ldq, Ks0 + (st ^ 1) * 16384);
+      load_sw_tile(Vg + (int64_t)(kt + 1) * TCQ * A.ldq, A.ldq, Vs0 + (st ^ 1) * 16384);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        tc_mma_bf16(tS, make_sdesc_sw128(smem_u32(Qs) + kk * 32, 16, 1024), make_sdesc_sw128(smem_u32(Ks) + kk * 32, 16, 1024),
+                    idS, kk > 0);
+      tc_commit(&bar[0]);
+    }
+    mbar_wait(&bar[0], (uint32_t)(kt & 1));
+    tc_fence_after();
+    float sv[64];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_ld16(tS + lane_off + hf * 64 + c * 16, sv + c * 16);
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      const int key = kt * TCQ + hf * 64 + j;
+      const float v = key <= q ? sv[j] * A.scale_log2 : -INFINITY;
+      sv[j] = v;
+      mx = fmaxf(mx, v);
+    }
+    xch[hf * 128 + row] = mx;
+    __syncthreads();
+    mx = fmaxf(xch[row], xch[128 + row]);
+    const float mn = fmaxf(m2, mx);
+    const float alpha = exp2f(m2 - mn);
+    m2 = mn;
+    l *= alpha;
+#pragma unroll
+    for (int g4 = 0; g4 < 16; ++g4) {
+      uint32_t kb = 0xFu;
+      if (A.thresh) {
+        const uint64_t qi = (rowbase + (uint64_t)(kt * TCQ + hf * 64 + 4 * g4)) >> 2;
+        const uint4 ph = philox4x32_10(make_uint4((uint32_t)qi, (uint32_t)(qi >> 32), A.site, pstep), pkey);
+        kb = ((ph.x >> 8) >= A.thresh ? 1u : 0u) | ((ph.y >> 8) >= A.thresh ? 2u : 0u) |
+             ((ph.z >> 8) >= A.thresh ? 4u : 0u) | ((ph.w >> 8) >= A.thresh ? 8u : 0u);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = 4 * g4 + e;
+        float p = exp2f(sv[j] - mn);
+        l += p;
+        if (A.thresh) p = ((kb >> e) & 1u) ? p * A.dscale : 0.0f;
+        sv[j] = p;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {  // this half's 64 keys = K-chunk hf of P
+      uint4 v;
+      v.x = pack2(sv[8 * c], sv[8 * c + 1]);
+      v.y = pack2(sv[8 * c + 2], sv[8 * c + 3]);
+      v.z = pack2(sv[8 * c + 4], sv[8 * c + 5]);
+      v.w = pack2(sv[8 * c + 6], sv[8 * c + 7]);
+      *reinterpret_cast<uint4*>(Ps + hf * 16384 + sw_off(row, c)) = v;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] *= alpha;
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        tc_mma_bf16(tO, make_sdesc_sw128(smem_u32(Ps) + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                    make_sdesc_sw128(smem_u32(Vs) + kk * 2048, 8192, 1024), idO, kk > 0);
+      tc_commit(&bar[1]);
+    }
+    mbar_wait(&bar[1], (uint32_t)(kt & 1));
+    tc_fence_after();
+    float pv[32];
+    tmem_ld16(tO + lane_off + hf * 32, pv);
+    tmem_ld16(tO + lane_off + hf * 32 + 16, pv + 16);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] += pv[i];
+  }
+  xch[hf * 128 + row] = l;  // (the last tile's reads of xch finished before the PV barrier)
+  __syncthreads();
+  const float lt = xch[row] + xch[128 + row];
+  const float inv = 1.0f / lt;
+  __nv_bfloat16* orow = ctx + (base + q) * ldc + h * HD + hf * 32;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint4 v;
+    v.x = pack2(o[8 * c] * inv, o[8 * c + 1] * inv);
+    v.y = pack2(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
+    v.z = pack2(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
+    v.w = pack2(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
+    *reinterpret_cast<uint4*>(orow + 8 * c) = v;
+  }
+  if (hf == 0) lse[(base + q) * A.nh + h] = m2 + log2f(lt);
+  tc_fence_before();
+  __syncthreads();
+  if (w == 0) tmem_dealloc(tmem, 256);
 }
 
 // D[row][h] = sum_c dO[row][h*64 + c] * O[row][h*64 + c]  (= rowsum(P o dP), the softmax VJP term)
@@ -581,6 +771,28 @@ int attn_fwd(cudaStream_t st, const void* qkv, int rows, int d, int nh, int seq,
     return TGP_E_UNSUPPORTED;
   }
   AttnArgs A = make_args(qkv, rows, d, nh, seq, row_global0, thresh, dscale, seed, step, site);
+  static const bool tc_on = [] {
+    const char* e = getenv("TGP_ATTN_TC");
+    return !(e && e[0] == '0');
+  }();
+  if (tc_on && seq % TCQ == 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+      if (e != cudaSuccess) {
+        set_error("attn_fwd_tc smem attribute: %s", cudaGetErrorString(e));
+        return TGP_E_CUDA;
+      }
+      attr = true;
+    }
+    attn_fwd_tc_kernel<<<dim3(seq / TCQ, nh, rows / seq), 256, TC_SMEM, st>>>(A, (__nv_bfloat16*)ctx, (int64_t)d, lse);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_error("attn_fwd_tc launch: %s", cudaGetErrorString(e));
+      return TGP_E_CUDA;
+    }
+    return 0;
+  }
   return launch("attn_fwd", attn_fwd_kernel, dim3(seq / TILE, nh, rows / seq), dim3(128), st, A,
                 (__nv_bfloat16*)ctx, (int64_t)d, lse);
 }
