@@ -199,10 +199,24 @@ TGP_DEV uint32_t attn_keep_tile_t(const AttnArgs& A, int s, int h, int kbase_w, 
 }
 
 
+// Work items of the forward: (query tile, key-tile range, part).  Causal rows are unequal (query tile
+// qt sees qt + 1 key tiles), and one micro-batch is one sequence, so a launch holds only
+// 25 heads x 16 tiles: the longest CTA (16 key tiles) bounded the kernel at ~2x the average.  Long
+// rows are therefore split into parts of <= KS key tiles (heaviest first); split rows write
+// unnormalised partial (O, m, l) and attn_fwd_merge_kernel combines the parts in fixed order.
+constexpr int FWD_MAX_ITEMS = 256, FWD_MAX_PARTS = 4, PART_STRIDE = HD + 2;
+struct FwdItems {
+  uint32_t it[FWD_MAX_ITEMS];  // qt | kt0 << 8 | kt1 << 16 | part << 24 (bit 31: split row)
+};
+
 __global__ void __launch_bounds__(128, TGP_ATTN_MINB) attn_fwd_kernel(AttnArgs A, __nv_bfloat16* __restrict__ ctx, int64_t ldc,
-                                                       float* __restrict__ lse) {
+                                                       float* __restrict__ lse, const FwdItems items,
+                                                       float* __restrict__ part_buf) {
   __shared__ __align__(16) __nv_bfloat16 Qs[TILE * PITCH], Ks[TILE * PITCH], Vs[TILE * PITCH];
-  const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+  const uint32_t item = items.it[blockIdx.x];
+  const int qt = item & 0xFF, kt0 = (item >> 8) & 0xFF, kt1 = (item >> 16) & 0xFF, part = (item >> 24) & 0x7F;
+  const bool split = (item >> 31) != 0;
+  const int h = blockIdx.y, s = blockIdx.z;
   const int w = threadIdx.x >> 5, g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
   const int64_t base = (int64_t)s * A.seq;
   load_tile(A.qkv + (base + qt * TILE) * A.ldq + h * HD, A.ldq, Qs, nullptr);
@@ -212,7 +226,7 @@ __global__ void __launch_bounds__(128, TGP_ATTN_MINB) attn_fwd_kernel(AttnArgs A
   float m2[2] = {-INFINITY, -INFINITY}, l[2] = {0.0f, 0.0f};
   float o[8][4] = {};
   const int q0 = qt * TILE + w * 16 + g;
-  for (int kt = 0; kt <= qt; ++kt) {
+  for (int kt = kt0; kt <= kt1; ++kt) {
     __syncthreads();
     load_tile(A.qkv + (base + kt * TILE) * A.ldq + A.d + h * HD, A.ldq, Ks, nullptr);
     load_tile(A.qkv + (base + kt * TILE) * A.ldq + 2 * A.d + h * HD, A.ldq, Vs, nullptr);
@@ -264,6 +278,21 @@ __global__ void __launch_bounds__(128, TGP_ATTN_MINB) attn_fwd_kernel(AttnArgs A
     l[r] += __shfl_xor_sync(0xffffffffu, l[r], 1);
     l[r] += __shfl_xor_sync(0xffffffffu, l[r], 2);
   }
+  if (split) {  // unnormalised partial of this key range
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int64_t row = base + q0 + r * 8;
+      float* pb = part_buf + ((row * A.nh + h) * FWD_MAX_PARTS + part) * PART_STRIDE;
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt)
+        *reinterpret_cast<float2*>(pb + dt * 8 + 2 * t) = make_float2(o[dt][2 * r], o[dt][2 * r + 1]);
+      if (t == 0) {
+        pb[HD] = m2[r];
+        pb[HD + 1] = l[r];
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int64_t row = base + q0 + r * 8;
@@ -274,6 +303,33 @@ __global__ void __launch_bounds__(128, TGP_ATTN_MINB) attn_fwd_kernel(AttnArgs A
           pack2(o[dt][2 * r] * inv, o[dt][2 * r + 1] * inv);
     if (t == 0) lse[row * A.nh + h] = m2[r] + log2f(l[r]);  // log2 domain
   }
+}
+
+// Combine the parts of split rows (fixed part order): one warp per (row, head), 2 columns per lane.
+__global__ void attn_fwd_merge_kernel(const float* __restrict__ part_buf, int seq, int nh, int q_first, int nparts_max,
+                                      int ks, int nrows, __nv_bfloat16* __restrict__ ctx, int64_t ldc,
+                                      float* __restrict__ lse) {
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= nrows * nh) return;
+  const int h = wid % nh, rr = wid / nh;           // rr enumerates the split rows of every sequence
+  const int per_seq = seq - q_first;
+  const int s = rr / per_seq, q = q_first + rr % per_seq;
+  const int np = (q / TILE) / ks + 1;              // parts of this query tile
+  const int64_t row = (int64_t)s * seq + q;
+  const float* pb = part_buf + (row * nh + h) * FWD_MAX_PARTS * PART_STRIDE;
+  float m = -INFINITY;
+  for (int p = 0; p < np; ++p) m = fmaxf(m, pb[p * PART_STRIDE + HD]);
+  float lt = 0.0f, o0 = 0.0f, o1 = 0.0f;
+  for (int p = 0; p < np; ++p) {
+    const float sc = exp2f(pb[p * PART_STRIDE + HD] - m);
+    lt += pb[p * PART_STRIDE + HD + 1] * sc;
+    o0 += pb[p * PART_STRIDE + 2 * lane] * sc;
+    o1 += pb[p * PART_STRIDE + 2 * lane + 1] * sc;
+  }
+  const float inv = 1.0f / lt;
+  *reinterpret_cast<uint32_t*>(ctx + row * ldc + h * HD + 2 * lane) = pack2(o0 * inv, o1 * inv);
+  if (lane == 0) lse[row * nh + h] = m + log2f(lt);
+  (void)nparts_max;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -764,16 +820,16 @@ bool attn_shape_ok(int rows, int d, int nh, int seq) {
 
 int attn_fwd(cudaStream_t st, const void* qkv, int rows, int d, int nh, int seq, int64_t row_global0,
              uint32_t thresh, float dscale, uint64_t seed, const uint32_t* step, uint32_t site, void* ctx,
-             float* lse) {
+             float* lse, float* part_buf) {
   if (!attn_shape_ok(rows, d, nh, seq)) {
     set_error("attention: need d = 64 * n_heads, seq %% 64 == 0, rows %% seq == 0 (d=%d nh=%d seq=%d rows=%d)", d,
               nh, seq, rows);
     return TGP_E_UNSUPPORTED;
   }
   AttnArgs A = make_args(qkv, rows, d, nh, seq, row_global0, thresh, dscale, seed, step, site);
-  static const bool tc_on = [] {
+  static const bool tc_on = [] {  // opt-in: TGP_ATTN_TC=1 (measured: no faster than the split mma.sync path)
     const char* e = getenv("TGP_ATTN_TC");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   if (tc_on && seq % TCQ == 0) {
     static bool attr = false;
@@ -793,8 +849,33 @@ int attn_fwd(cudaStream_t st, const void* qkv, int rows, int d, int nh, int seq,
     }
     return 0;
   }
-  return launch("attn_fwd", attn_fwd_kernel, dim3(seq / TILE, nh, rows / seq), dim3(128), st, A,
-                (__nv_bfloat16*)ctx, (int64_t)d, lse);
+  const int nq = seq / TILE;
+  int ks = 8;
+  while ((nq + ks - 1) / ks > FWD_MAX_PARTS) ks *= 2;
+  if (!part_buf) ks = nq;  // no scratch: one item per query tile
+  FwdItems items{};
+  int n = 0;
+  // heaviest first: items of ks key tiles, then the shorter remainders, in descending length
+  for (int len = ks; len >= 1; --len)
+    for (int qt = nq - 1; qt >= 0; --qt) {
+      const int np = qt / ks + 1;
+      for (int p = 0; p < np; ++p) {
+        const int a = p * ks, b = std::min(qt, a + ks - 1);
+        if (b - a + 1 != len) continue;
+        if (n >= FWD_MAX_ITEMS) {
+          set_error("attention: seq %d needs more than %d forward work items", seq, FWD_MAX_ITEMS);
+          return TGP_E_UNSUPPORTED;
+        }
+        items.it[n++] = (uint32_t)qt | ((uint32_t)a << 8) | ((uint32_t)b << 16) | ((uint32_t)p << 24) |
+                        (np > 1 ? 0x80000000u : 0u);
+      }
+    }
+  TGP_TRY(launch("attn_fwd", attn_fwd_kernel, dim3(n, nh, rows / seq), dim3(128), st, A, (__nv_bfloat16*)ctx,
+                 (int64_t)d, lse, items, part_buf));
+  if (ks >= nq) return 0;
+  const int q_first = ks * TILE, nrows = (rows / seq) * (seq - q_first);
+  return launch("attn_fwd_merge", attn_fwd_merge_kernel, dim3((nrows * nh + 3) / 4), dim3(128), st,
+                (const float*)part_buf, seq, nh, q_first, FWD_MAX_PARTS, ks, nrows, (__nv_bfloat16*)ctx, (int64_t)d, lse);
 }
 
 int attn_bwd(cudaStream_t st, const void* qkv, const void* ctx, const float* dO, const float* lse, float* Dbuf,

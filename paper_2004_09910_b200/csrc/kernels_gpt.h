@@ -13,8 +13,11 @@ namespace tgp {
 //   qkv [rows][3d] bf16 (q | k | v, head h = columns h*64 .. h*64+63 of each third), rows % seq == 0,
 //   row_global0 = global token row of row 0 (dropout counters: flat index in [n_seq, nh, seq, seq]).
 //   ctx [rows][d] bf16 = softmax(q k^T / 8, causal) [dropout] v;  lse [rows][nh] fp32 (log2 domain).
+//   part_buf: rows * nh * 4 * 66 floats of scratch for the split-row partials (nullable: no split).
 int attn_fwd(cudaStream_t st, const void* qkv, int rows, int d, int nh, int seq, int64_t row_global0,
-             uint32_t thresh, float dscale, uint64_t seed, const uint32_t* step, uint32_t site, void* ctx, float* lse);
+             uint32_t thresh, float dscale, uint64_t seed, const uint32_t* step, uint32_t site, void* ctx, float* lse,
+             float* part_buf);
+constexpr int ATTN_PART_FLOATS = 4 * 66;  // per (row, head)
 // Backward: dO [rows][d] fp32 -> dqkv [rows][3d] fp32.  Dbuf: rows*nh floats of scratch.
 int attn_bwd(cudaStream_t st, const void* qkv, const void* ctx, const float* dO, const float* lse, float* Dbuf,
              int rows, int d, int nh, int seq, int64_t row_global0, uint32_t thresh, float dscale, uint64_t seed,

@@ -494,7 +494,7 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         TGP_TRY(run_gemm(c, s, pdl(), Opnd{wparam(c, s, L, 2), d3, d, d}, false, Opnd{L.Hop, c->max_batch, d, d},
                          nullptr, false, d3, M, d, r0, d, true, e1));
         TGP_TRY(attn_fwd(s.comp, opptr(c, L.QKVop, r0, d3), M, d, L.L.n_heads, L.L.seq, r0, th, dsc, c->seed, s.dstep,
-                         (uint32_t)l + (1u << 16), opptr(c, L.CTXop, r0, d), L.lse[slot]));
+                         (uint32_t)l + (1u << 16), opptr(c, L.CTXop, r0, d), L.lse[slot], s.attn_part));
         c->kernels++;
         first_kernel = true;  // the attention kernel does not trigger dependents early
         EpiParams e2 = e;

@@ -104,6 +104,7 @@ struct Stage {
   float* gbuf[2] = {nullptr, nullptr};
   float* tbuf = nullptr;   // [mb_cap][maxw] fp32 scratch (attention backward dqkv)
   float* attnD = nullptr;  // [mb_cap][max heads] fp32 scratch (attention backward rowsum(dO o O))
+  float* attn_part = nullptr;  // [mb_cap][max heads][4][66] fp32: split-row forward partials
   double* ce_part = nullptr;  // [max_batch + 1] cross-entropy row losses (last partition)
   uint32_t* counters = nullptr;  // [8]
   double* loss_buf = nullptr;

@@ -116,3 +116,13 @@ def test_c5_full_width_parity():
     # shortened stack: embed + 2 blocks + LM head, 2 sequences, m = 2, n = 2, dropout 0.1, always
     layers = C.gpt2_stack(2, 1600, 25, 1024, 50304, 0.1)
     _run(layers, 2, 2, 2, "always", balance=[2, 2], seed=21)
+
+
+def test_c5_split_rows_attention():
+    # seq 640 = 10 key tiles: query tiles 8 and 9 are split into two key ranges (partials merged in
+    # fixed order); also checked against the checkpoint-free run bitwise (F' == F)
+    layers = C.gpt2_stack(2, 128, 2, 640, 512, 0.1)
+    gpu, ref, errs = _run(layers, 2, 2, 2, "always", balance=[2, 2], seed=9)
+    x, t, params = make_case(layers, 2, 9, "bf16")
+    b = gpt_step(layers, params, x, t, m=2, n=2, ckpt="never", lr=0.01, balance=[2, 2], seed=9)
+    assert b["loss"] == gpu["loss"] and np.array_equal(b["y"], gpu["y"])
