@@ -814,6 +814,9 @@ int launch(const char* name, Kern k, dim3 grid, dim3 block, cudaStream_t st, Arg
 
 }  // namespace
 
+static int g_attn_tc = -1;  // -1: environment (TGP_ATTN_TC), else option "attn_tc"
+void attn_set_tc(int on) { g_attn_tc = on; }
+
 bool attn_shape_ok(int rows, int d, int nh, int seq) {
   return nh > 0 && d == nh * HD && seq % TILE == 0 && seq > 0 && rows % seq == 0;
 }
@@ -827,10 +830,11 @@ int attn_fwd(cudaStream_t st, const void* qkv, int rows, int d, int nh, int seq,
     return TGP_E_UNSUPPORTED;
   }
   AttnArgs A = make_args(qkv, rows, d, nh, seq, row_global0, thresh, dscale, seed, step, site);
-  static const bool tc_on = [] {  // opt-in: TGP_ATTN_TC=1 (measured: no faster than the split mma.sync path)
+  static const bool tc_env = [] {  // opt-in: TGP_ATTN_TC=1 (measured: no faster than the split mma.sync path)
     const char* e = getenv("TGP_ATTN_TC");
     return e && e[0] == '1';
   }();
+  const bool tc_on = g_attn_tc < 0 ? tc_env : g_attn_tc != 0;
   if (tc_on && seq % TCQ == 0) {
     static bool attr = false;
     if (!attr) {

@@ -23,6 +23,9 @@ int attn_bwd(cudaStream_t st, const void* qkv, const void* ctx, const float* dO,
              int rows, int d, int nh, int seq, int64_t row_global0, uint32_t thresh, float dscale, uint64_t seed,
              const uint32_t* step, uint32_t site, float* dqkv);
 bool attn_shape_ok(int rows, int d, int nh, int seq);
+// Select the tcgen05 forward for seq % 128 == 0 (1), the mma.sync one (0), or the TGP_ATTN_TC
+// environment default (-1).  Process-wide (option "attn_tc").
+void attn_set_tc(int on);
 // y[r] = wte[id_r] + wpe[(row_global0 + r) % seq] [dropout]; ids = token ids stored as fp32 (stride ldi)
 int embed_fwd(cudaStream_t st, const float* ids, int64_t ldi, int rows, const float* wte, const float* wpe, int d,
               int seq, int64_t row_global0, uint32_t thresh, float dscale, uint64_t seed, const uint32_t* step,

@@ -126,3 +126,20 @@ def test_c5_split_rows_attention():
     x, t, params = make_case(layers, 2, 9, "bf16")
     b = gpt_step(layers, params, x, t, m=2, n=2, ckpt="never", lr=0.01, balance=[2, 2], seed=9)
     assert b["loss"] == gpu["loss"] and np.array_equal(b["y"], gpu["y"])
+
+
+def test_c5_tcgen05_attention_forward():
+    # the tcgen05 attention forward (option attn_tc, seq % 128 == 0) against the oracle
+    layers = C.gpt2_stack(2, 128, 2, 256, 512, 0.1)
+    x, t, params = make_case(layers, 2, 4, "bf16")
+    try:
+        gpu = gpt_step(layers, params, x, t, m=2, n=2, ckpt="always", lr=0.01, balance=[2, 2], seed=4,
+                       options={"attn_tc": 1})
+    finally:
+        from paper_2004_09910_b200 import Pipeline  # reset the process-wide switch
+        P = Pipeline(layers, chunks=2, devices=[0, 0], balance=[2, 2], max_batch=x.shape[0], dtype="bf16")
+        P.set_option("attn_tc", -1)
+        P.close()
+    ref = oracle_step(layers, params, x, t, lr=0.01, m=2, seed=4, step=0)
+    errs, bad = compare(gpu, ref, params, 2e-2, 0.01)
+    assert not bad, bad
