@@ -336,12 +336,21 @@ __global__ void __launch_bounds__(128) colwise_kernel(const float* __restrict__ 
       if (r >= rows) break;
       float4 v = *reinterpret_cast<const float4*>(src + (int64_t)r * lds + c0);
       float vv[4] = {v.x, v.y, v.z, v.w};
+      uint32_t kw[4] = {0u, 0u, 0u, 0u};
+      if (thresh) {
+        // the 4 elements of this float4 share one Philox call: their flat index (row * d + c0 + e,
+        // d % 4 == 0, c0 % 4 == 0) has the same counter q = idx >> 2 and picks word e (O8)
+        const uint64_t q = ((uint64_t)(row0 + r) * (uint64_t)d + (uint64_t)c0) >> 2;
+        const uint4 o = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), site, st),
+                                      make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+        kw[0] = o.x;
+        kw[1] = o.y;
+        kw[2] = o.z;
+        kw[3] = o.w;
+      }
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        if (thresh) {
-          const uint64_t idx = (uint64_t)(row0 + r) * (uint64_t)d + (uint64_t)(c0 + e);
-          vv[e] = dropout_keep(seed, st, site, idx, thresh) ? vv[e] * scale : 0.0f;
-        }
+        if (thresh) vv[e] = (kw[e] >> 8) >= thresh ? vv[e] * scale : 0.0f;
         if (act) vv[e] *= act_df(act, z[(int64_t)r * d + c0 + e]);
       }
       v = make_float4(vv[0], vv[1], vv[2], vv[3]);
