@@ -755,43 +755,51 @@ __global__ void embed_wpe_kernel(const float* __restrict__ dE, int rows, int d, 
 // ------------------------------------------------------------------------------- cross-entropy
 __global__ void ce_row_kernel(const float* __restrict__ y, int64_t ldy, const int* __restrict__ tgt, int V, int T,
                               float* __restrict__ dy, double* __restrict__ part) {
-  __shared__ float sh[32];
-  __shared__ float bc;
+  // one pass for the row maximum and the rescaled exponential sum (online softmax, per thread then a
+  // fixed-order combination), one pass writing dy: 2 reads of the logits instead of 3
+  __shared__ float shm[32], shs[32];
+  __shared__ float bm, bs;
   const int r = blockIdx.x;
   const float* yr = y + (int64_t)r * ldy;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  float mx = -INFINITY;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, yr[c]);
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) sh[w] = mx;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float m = sh[0];
-    for (int i = 1; i < nw; ++i) m = fmaxf(m, sh[i]);
-    bc = m;
+  float m = -INFINITY, se = 0.0f;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    const float v = yr[c];
+    if (v > m) {
+      se = se * __expf(m - v) + 1.0f;
+      m = v;
+    } else {
+      se += __expf(v - m);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, se, o);
+    const float mn = fmaxf(m, m2);
+    se = (m == -INFINITY ? 0.0f : se * __expf(m - mn)) + (m2 == -INFINITY ? 0.0f : s2 * __expf(m2 - mn));
+    m = mn;
+  }
+  if (lane == 0) {
+    shm[w] = m;
+    shs[w] = se;
   }
   __syncthreads();
-  mx = bc;
-  float se = 0.0f;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) se += __expf(yr[c] - mx);
-  for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-  __syncthreads();
-  if (lane == 0) sh[w] = se;
-  __syncthreads();
   if (threadIdx.x == 0) {
-    float s = 0.0f;
-    for (int i = 0; i < nw; ++i) s += sh[i];  // fixed order
-    bc = s;
+    float mm = shm[0];
+    for (int i = 1; i < nw; ++i) mm = fmaxf(mm, shm[i]);
+    float ss = 0.0f;
+    for (int i = 0; i < nw; ++i) ss += shm[i] == -INFINITY ? 0.0f : shs[i] * __expf(shm[i] - mm);  // fixed order
+    bm = mm;
+    bs = ss;
   }
   __syncthreads();
-  se = bc;
+  const float mx = bm, sum = bs;
   const int tg = tgt[r];
-  const float inv = 1.0f / se, invT = 1.0f / (float)T;
+  const float inv = 1.0f / sum, invT = 1.0f / (float)T;
   for (int c = threadIdx.x; c < V; c += blockDim.x) {
     const float p = __expf(yr[c] - mx) * inv;
     dy[(int64_t)r * ldy + c] = (p - (c == tg ? 1.0f : 0.0f)) * invT;
   }
-  if (threadIdx.x == 0) part[r] = (double)mx + log((double)se) - (double)yr[tg];
+  if (threadIdx.x == 0) part[r] = (double)mx + log((double)sum) - (double)yr[tg];
 }
 __global__ void ce_final_kernel(const double* part, int T, double* loss) {
   if (threadIdx.x == 0) {
