@@ -225,6 +225,10 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *             weight-streaming kernel per task (task_stream.cu; default 1 where eligible)
  *  "dw_persistent" deferred weight gradients through the persistent 128x128-tile dW kernel (default 1)
  *  "stream_poll_ns" back-off of the stream kernel's dependency polling loops, ns (default 32)
+ *  "gemm_wide" per-micro-batch GEMMs with >= 256 rows through the persistent gemm_wide kernel
+ *             (default 1; 0 = the one-tile-per-CTA GEMM)
+ *  "attn_tc"  PROCESS-WIDE: 1 = tcgen05 attention forward where seq % 128 == 0, 0 = mma.sync,
+ *             -1 = the TGP_ATTN_TC environment default (off)
  * Table 1 ablation toggles (results are bitwise those of the default -- only the
  * issue order and the copy path change).  Need every partition in this process, and not between
  * forward and backward (TGP_E_UNSUPPORTED / TGP_E_STATE):
