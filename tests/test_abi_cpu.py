@@ -87,6 +87,35 @@ def test_create_validates_before_touching_cuda(L):
         L.Pipeline(layers, chunks=2, devices=[0], balance=[len(layers)], max_batch=4, dtype="bf16")
 
 
+def test_create_validates_gpt2_layers(L):
+    # GPT-2-shaped kinds (C5): validation happens before any CUDA call, so it is testable here
+    from synth import configs as C
+
+    def make(layers, **kw):
+        args = dict(chunks=2, devices=[0], balance=[len(layers)], max_batch=2 * 64, dtype="bf16")
+        args.update(kw)
+        return L.Pipeline(layers, **args)
+
+    ok = C.gpt2_stack(2, 128, 2, 64, 512, 0.1)
+    cases = []
+    bad = [dict(L) for L in ok]
+    bad[1]["n_heads"] = 3                           # d != 64 * n_heads
+    cases.append((bad, {}, "(-1)"))
+    bad = [dict(L) for L in ok]
+    bad[1]["seq"] = bad[2]["seq"] = 96              # seq % 64 != 0
+    cases.append((bad, {}, "(-1)"))
+    bad = [dict(L) for L in ok]
+    bad[0], bad[1] = bad[1], bad[0]                 # embedding not at layer 0
+    cases.append((bad, {}, "(-1)"))
+    cases.append((ok, dict(max_batch=100), "(-1)"))  # max_batch not whole sequences
+    cases.append((ok, dict(chunks=3), "(-1)"))       # more micro-batches than sequences
+    cases.append((ok, dict(dtype="fp32"), "(-5)"))   # bf16 only
+    for layers, kw, code in cases:
+        with pytest.raises(L.TgpError) as ei:
+            make(layers, **kw)
+        assert code in str(ei.value), (kw, str(ei.value))
+
+
 def test_no_cpu_fallback(L):
     # a valid pipeline on a machine without a GPU must fail loudly (TGP_E_CUDA), never fall back
     import torch
