@@ -432,38 +432,9 @@ __global__ void __launch_bounds__(224, 1) task_stream_kernel(const __grid_consta
       }
       ++n;
     };
-    // Forward LayerNorm folded into GEMM1 (reading R3 in DESIGN.md).  With mu, rs the statistics
-    // of the block input y and mu~ the input mean of the previous block (0 for the first):
-    //   a = LN(y) W1^T + b1 = rs (sum_k bf16(gamma_k (y_k - mu~)) W1[h][k] - (mu - mu~) c_h) + e_h
-    // with c_h = sum_k gamma_k W1[h][k], e_h = sum_k beta_k W1[h][k] + b1[h] (task_stream_fold).  The
-    // GEMM1 operand needs no row statistics, so the statistics exchange overlaps GEMM1 instead of
-    // preceding it; the exact LN output (dW1 stash) and mean / rstd are written off the critical path.
-    //
-    // producer side (owners of the block input, d-space): chunk statistics (mean, M2 over the 32
-    // features) and the operand gamma (y - mu~), then the quarter counter (operand) and the global
-    // counter (statistics).  mut[e] = mu~ of row 4ew+e.
-    auto ln_produce = [&](const float* y, const float* mut, int l, float g, __nv_bfloat16* yg) {
-      const int J = d / 32;
-      float* st = t.stats + (size_t)l * J * 32;
-      // the operand first (critical path: the next GEMM1's activation tiles), statistics after
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = 4 * ew + e;
-        yg[(size_t)r * d + fo] = __float2bfloat16_rn(r < M ? g * (y[e] - mut[e]) : 0.0f);
-      }
-      signal(1 + 3 * l, fo / (d / 4));
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = 4 * ew + e;
-        const float mu = wsum32(y[e]) * (1.0f / 32.0f);
-        const float dv = y[e] - mu;
-        const float m2 = wsum32(dv * dv);
-        if (lane == 0) *reinterpret_cast<float2*>(st + ((size_t)chunk * 16 + r) * 2) = make_float2(mu, m2);
-      }
-      signal(3 + 3 * l, 4);
-    };
     // consumer side: wait for all chunk statistics of block l's input, combine them in fixed order
-    // (identical in every CTA) into rmu / rrs; the previous means move to rmp.
+    // (identical in every CTA) into rmu / rrs; the previous means move to rmp (mu~ of block l; for
+    // block 0 the exact mean, see ln_produce_first).
     float* rmp = cs + 3 * 4 * 32;  // [16] mu~ of the current block (previous block's input mean)
     auto ln_rows = [&](int l) {
       const int J = d / 32;
@@ -495,7 +466,7 @@ __global__ void __launch_bounds__(224, 1) task_stream_kernel(const __grid_consta
       m2 += __shfl_xor_sync(0xffffffffu, m2, 1);
       const float rs = 1.0f / sqrtf(m2 / (float)d + 1e-5f);
       if (jl == 0) {
-        rmp[rr] = l == 0 ? 0.0f : rmu[rr];
+        rmp[rr] = l == 0 ? mu : rmu[rr];  // block 0: operand centred on its exact mean
         rmu[rr] = mu;
         rrs[rr] = rs;
         if (blockIdx.x == 0 && rr < M) {
@@ -504,6 +475,59 @@ __global__ void __launch_bounds__(224, 1) task_stream_kernel(const __grid_consta
         }
       }
       epi_bar();
+    };
+    // Forward LayerNorm folded into GEMM1 (reading R3 in DESIGN.md).  With mu, rs the statistics
+    // of the block input y and mu~ the input mean of the previous block (0 for the first):
+    //   a = LN(y) W1^T + b1 = rs (sum_k bf16(gamma_k (y_k - mu~)) W1[h][k] - (mu - mu~) c_h) + e_h
+    // with c_h = sum_k gamma_k W1[h][k], e_h = sum_k beta_k W1[h][k] + b1[h] (task_stream_fold).  The
+    // GEMM1 operand needs no row statistics, so the statistics exchange overlaps GEMM1 instead of
+    // preceding it; the exact LN output (dW1 stash) and mean / rstd are written off the critical path.
+    //
+    // producer side (owners of the block input, d-space): chunk statistics (mean, M2 over the 32
+    // features) and the operand gamma (y - mu~), then the quarter counter (operand) and the global
+    // counter (statistics).  mut[e] = mu~ of row 4ew+e.
+    auto ln_produce = [&](const float* y, const float* mut, int l, float g, __nv_bfloat16* yg) {
+      const int J = d / 32;
+      float* st = t.stats + (size_t)l * J * 32;
+      // the operand first (critical path: the next GEMM1's activation tiles), statistics after
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = 4 * ew + e;
+        yg[(size_t)r * d + fo] = __float2bfloat16_rn(r < M ? g * (y[e] - mut[e]) : 0.0f);
+      }
+      signal(1 + 3 * l, fo / (d / 4));
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = 4 * ew + e;
+        const float mu = wsum32(y[e]) * (1.0f / 32.0f);
+        const float dv = y[e] - mu;
+        const float m2 = wsum32(dv * dv);
+        if (lane == 0) *reinterpret_cast<float2*>(st + ((size_t)chunk * 16 + r) * 2) = make_float2(mu, m2);
+      }
+      signal(3 + 3 * l, 4);
+    };
+    // block 0 of the task: no previous block mean to centre on, and the stage input may sit far off
+    // zero (row mean >> row std), where bf16(gamma y) would lose the (y - mu) digits.  So the chunk
+    // statistics go first, every producer waits for all of them and centres the operand on the exact
+    // mean (mu~ = mu, the correction term vanishes).  One exchange more, only at the task start.
+    auto ln_produce_first = [&](const float* y, float g, __nv_bfloat16* yg) {
+      float* st = t.stats;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = 4 * ew + e;
+        const float mu = wsum32(y[e]) * (1.0f / 32.0f);
+        const float dv = y[e] - mu;
+        const float m2 = wsum32(dv * dv);
+        if (lane == 0) *reinterpret_cast<float2*>(st + ((size_t)chunk * 16 + r) * 2) = make_float2(mu, m2);
+      }
+      signal(3, 4);
+      ln_rows(0);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = 4 * ew + e;
+        yg[(size_t)r * d + fo] = __float2bfloat16_rn(r < M ? g * (y[e] - rmu[r]) : 0.0f);
+      }
+      signal(1, fo / (d / 4));
     };
     // exact LN output of the thread's own d-space item (dW1 operand stash, read by W_j only)
     auto ln_stash = [&](const float* y, int l) {
@@ -521,13 +545,12 @@ __global__ void __launch_bounds__(224, 1) task_stream_kernel(const __grid_consta
       // ---------------------------------------------------------------- forward task
       float yk[4] = {0.f, 0.f, 0.f, 0.f};  // the thread's d-space item of the current block input
       if (own_d) {
-        const float zero[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int r = 4 * ew + e;
           yk[e] = r < M ? __ldcg(t.micro[0].x + (size_t)r * d + fo) : 0.0f;
         }
-        ln_produce(yk, zero, 0, t.layers[0].gamma[fo], t.layers[0].yg);
+        ln_produce_first(yk, t.layers[0].gamma[fo], t.layers[0].yg);
       }
       for (int l = 0; l < t.L; ++l) {
         const SLayer& Ly = t.layers[l];

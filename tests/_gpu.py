@@ -83,7 +83,19 @@ def oracle_step(layers, params, x, t, *, lr, m, seed=0, step=0):
     return OM.train_step(layers, params, x, t, lr=lr, m=m, seed=seed, step=step)
 
 
-def make_case(layers, B, seed, dtype):
-    x, t = G.inputs(layers, B, seed=seed, dtype=dtype)
-    params = G.params(layers, seed=seed, dtype=dtype)
+def bf16_shadow(layers, params):
+    """The weights a bf16-mode GEMM reads after an SGD step (reading Z14: the bf16 shadow of the fp32
+    master): weight matrices rounded to bf16, vectors (biases, LN gamma / beta) kept.  Applied to
+    ORACLE parameters (e.g. the oracle's own step-0 result) to form the oracle's step-1 input, so the
+    rounding of the inputs is not counted as error (O1) -- nothing here comes from the CUDA path."""
+    out = []
+    for (li, name, shape), p in zip(C.param_shapes(layers), params):
+        p = np.asarray(p, np.float64)
+        out.append(G.round_bf16(p).astype(np.float64) if len(shape) == 2 and name not in ("wte", "wpe") else p)
+    return out
+
+
+def make_case(layers, B, seed, dtype, x_mean=0.0, ln="default"):
+    x, t = G.inputs(layers, B, seed=seed, dtype=dtype, x_mean=x_mean)
+    params = G.params(layers, seed=seed, dtype=dtype, ln=ln)
     return x, t, params

@@ -8,16 +8,16 @@ import pytest
 
 from synth import configs as C
 
-from _gpu import compare, gpu_step, make_case, oracle_step
+from _gpu import bf16_shadow, compare, gpu_step, make_case, oracle_step
 
 pytestmark = pytest.mark.gpu
 TOL = 2e-2
 
 
-def _run(layers, B, m, n, ckpt, seed, options=None, balance=None):
-    x, t, params = make_case(layers, B, seed, "bf16")
+def _run(layers, B, m, n, ckpt, seed, options=None, balance=None, x_mean=0.0, ln="default", steps=1):
+    x, t, params = make_case(layers, B, seed, "bf16", x_mean=x_mean, ln=ln)
     g, P = gpu_step(layers, params, x, t, m=m, n=n, ckpt=ckpt, dtype="bf16", lr=0.05, seed=seed, balance=balance,
-                    options=options)
+                    options=options, steps=steps)
     return x, t, params, g, P
 
 
@@ -86,6 +86,57 @@ def test_stream_full_c2_width_parity():
     x, t, params, g, P = _run(layers, 512, 32, 1, "except_last", 1234)
     P.close()
     ref = oracle_step(layers, params, x, t, lr=0.05, m=32, seed=1234, step=0)
+    errs, bad = compare(g, ref, params, TOL, 0.05)
+    assert not bad, bad
+
+
+def test_full_c2_bench_config_parity():
+    # VERDICT r1 "next" 1: the EXACT bench configuration (32 x 4096 RESMLP, B = 512, m = 32,
+    # except_last, bf16, stream kernel: L = 32 blocks in one launch, 64 phases) against the fp64
+    # oracle -- loss, y, dx, every gradient and every delta-theta at 2e-2 normwise (reading Z15)
+    layers = C.resmlp_stack(32, 4096)
+    x, t, params = make_case(layers, 512, 1234, "bf16")
+    g, P = gpu_step(layers, params, x, t, m=32, n=1, ckpt="except_last", dtype="bf16", lr=0.05, seed=1234)
+    assert P.stream_enabled(0)
+    P.close()
+    ref = oracle_step(layers, params, x, t, lr=0.05, m=32, seed=1234, step=0)
+    errs, bad = compare(g, ref, params, TOL, 0.05)
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("x_mean", [4.0, 32.0])
+def test_stream_offcenter_inputs_parity(x_mean):
+    # VERDICT r1 "weak" 2: the LayerNorm folds of the stream kernel (DESIGN R3 forward, R4 backward)
+    # change which value is rounded to bf16; off the zero-mean regime (row mean >> row std, wide
+    # gamma / beta) the result must still meet 2e-2 normwise.  x ~ N(mu, 1), gamma ~ U(0.25, 4),
+    # beta ~ N(0, 1), d = H = 4096, 4 blocks, 16-row micro-batches, dropout, two steps (the fold
+    # vectors are recomputed after the SGD step)
+    layers = C.resmlp_stack(4, 4096, dropout=0.1)
+    B, m, lr, seed = 64, 4, 0.05, 31
+    x, t, params = make_case(layers, B, seed, "bf16", x_mean=x_mean, ln="wide")
+    g, P = gpu_step(layers, params, x, t, m=m, n=1, ckpt="except_last", dtype="bf16", lr=lr, seed=seed, steps=2)
+    assert P.stream_enabled(0)
+    P.close()
+    ref0 = oracle_step(layers, params, x, t, lr=lr, m=m, seed=seed, step=0)
+    errs, bad = compare(g[0], ref0, params, TOL, lr)
+    assert not bad, ("step 0", bad)
+    # step 1 runs on the bf16 shadow of the updated master weights (Z14); the oracle gets the same
+    # rounding of ITS step-0 weights (profiles/diag/offcenter_diag.py: unrounded, both the stream and
+    # the per-layer path miss the last block's dbeta by 2.5e-2 at x_mean 4 -- the bf16 weight
+    # rounding, not the folds)
+    p1 = bf16_shadow(layers, ref0["params"])
+    ref1 = oracle_step(layers, p1, x, t, lr=lr, m=m, seed=seed, step=1)
+    errs, bad = compare(g[1], ref1, p1, TOL, lr, gpu_base=g[0]["params"])
+    assert not bad, ("step 1", bad)
+
+
+def test_stream_offcenter_two_partitions():
+    # off-centre inputs through a partition boundary (the second partition's first block has mu~ = 0
+    # in the stream kernel's forward fold) and the ragged tail
+    layers = C.resmlp_stack(4, 1024, hidden=2048)
+    x, t, params, g, P = _run(layers, 60, 4, 2, "always", 32, balance=[2, 2], x_mean=16.0, ln="wide")
+    P.close()
+    ref = oracle_step(layers, params, x, t, lr=0.05, m=4, seed=32, step=0)
     errs, bad = compare(g, ref, params, TOL, 0.05)
     assert not bad, bad
 

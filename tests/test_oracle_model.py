@@ -79,7 +79,7 @@ def test_finite_differences(mk, m):
 
 
 # ---------------------------------------------------------------- torch fp64 cross-check
-def torch_step(layers, params, x, t, m, seed, step):
+def torch_step(layers, params, x, t, m, seed, step, lr=None):
     P = [torch.tensor(np.asarray(p, np.float64), requires_grad=True) for p in params]
     X = torch.tensor(np.asarray(x, np.float64), requires_grad=True)
     B = X.shape[0]
@@ -128,7 +128,13 @@ def torch_step(layers, params, x, t, m, seed, step):
     T = torch.tensor(np.asarray(t, np.float64))
     loss = ((h - T) ** 2).sum() / T.numel()
     loss.backward()
-    return float(loss.detach()), [p.grad.numpy() for p in P], X.grad.numpy(), running
+    grads = [p.grad.numpy().copy() for p in P]
+    if lr is None:
+        return float(loss.detach()), grads, X.grad.numpy(), running
+    # the optimizer step by an independent library routine: plain SGD, no momentum / decay
+    opt = torch.optim.SGD(P, lr=lr, momentum=0.0, weight_decay=0.0)
+    opt.step()
+    return float(loss.detach()), grads, X.grad.numpy(), running, [p.detach().numpy() for p in P]
 
 
 @pytest.mark.parametrize("name", ["C1", "C2small", "C2small_drop", "C4small", "BN"])
@@ -148,7 +154,7 @@ def test_vs_torch_autograd(name):
     x, t = G.inputs(layers, B, seed=5)
     params = G.params(layers, seed=5)
     r = M.train_step(layers, params, x, t, lr=0.1, m=m, seed=77, step=2)
-    loss, grads, dx, running = torch_step(layers, params, x, t, m, 77, 2)
+    loss, grads, dx, running, new = torch_step(layers, params, x, t, m, 77, 2, lr=0.1)
     assert abs(r["loss"] - loss) <= 1e-12 * abs(loss)
     scale = max(np.max(np.abs(gt)) for gt in grads)  # BN makes the preceding bias grad exactly 0
     for g, gt in zip(r["grads"], grads):
@@ -156,8 +162,10 @@ def test_vs_torch_autograd(name):
     assert nwise(r["dx"], dx) <= 1e-11
     for (rm, rv), (tm, tv) in zip(r["bn"], running):
         assert nwise(rm, tm) <= 1e-12 and nwise(rv, tv) <= 1e-12
-    for p, pn, g in zip(params, r["params"], r["grads"]):
-        assert np.allclose(pn, np.asarray(p, np.float64) - 0.1 * g, rtol=0, atol=1e-15)
+    # the SGD update pinned against torch.optim.SGD (VERDICT r1 "weak" 3): theta' and delta-theta
+    for p, pn, pt in zip(params, r["params"], new):
+        p = np.asarray(p, np.float64)
+        assert np.max(np.abs(pn - pt)) <= 1e-11 * max(np.max(np.abs(pt - p)), 1e-3 * scale * 0.1)
 
 
 # ---------------------------------------------------------------- emulator (O10)
