@@ -241,10 +241,7 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  * Test-only negative controls (never used on the product path):
  *  "test_poison"        fill the forward receive slabs with NaN before each forward call
  *  "test_skip_wait"     drop the receive waits of partition `value` (-1 = none)
- *  "test_delay_push_us" delay every push on its copy stream by `value` microseconds
- *  "test_stream_variant" timing experiments on the stream kernel (bit 0: ignore data dependencies,
- *                       bit 1: contiguous weight tiles, bit 2: no L2 promotion, bit 3: evict-normal
- *                       weights; bits 0 / 1 make the results garbage) */
+ *  "test_delay_push_us" delay every push on its copy stream by `value` microseconds */
 tgp_status tgp_set_option(tgp_ctx* ctx, const char* name, int64_t value);
 
 const char* tgp_last_error(void);

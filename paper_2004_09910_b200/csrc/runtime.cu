@@ -246,18 +246,14 @@ static int st_build_desc(tgp_ctx* c, Stage& s, int B) {
     memset(&P, 0, sizeof(P));
     const void* w1 = wparam(c, s, Ly, 2);
     const void* w2 = wparam(c, s, Ly, 4);
-    const bool promo = !(c->st_flags & 4);  // test_stream_variant bit 2: no L2 256-byte promotion
-    if (!make_map(&P.w1k, TcMat{w1, H, d, d}, 64, 128, promo) || !make_map(&P.w2k, TcMat{w2, d, H, H}, 64, 128, promo) ||
-        !make_map(&P.w2m, TcMat{w2, d, H, H}, 64, 64, promo) || !make_map(&P.w1m, TcMat{w1, H, d, d}, 64, 64, promo) ||
-        !make_map(&P.w1c, TcMat{w1, (int64_t)H * d / 64, 64, 64}, 64, 128, promo) ||
-        !make_map(&P.w2c, TcMat{w2, (int64_t)H * d / 64, 64, 64}, 64, 128, promo) ||
-        !make_map(&P.hop, TcMat{Ly.Hop, c->max_batch, d, d}, 64, 16) ||
+    if (!make_map(&P.w1k, TcMat{w1, H, d, d}, 64, 128) || !make_map(&P.w2k, TcMat{w2, d, H, H}, 64, 128) ||
+        !make_map(&P.w2m, TcMat{w2, d, H, H}, 64, 64) || !make_map(&P.w1m, TcMat{w1, H, d, d}, 64, 64) ||
         !make_map(&P.gop, TcMat{Ly.Gop, c->max_batch, H, H}, 64, 16) ||
-        !make_map(&P.dyop, TcMat{Ly.dYop, c->max_batch, d, d}, 64, 16) ||
-        !make_map(&P.daop, TcMat{Ly.dAop, c->max_batch, H, H}, 64, 16))
+        !make_map(&P.daop, TcMat{Ly.dAop, c->max_batch, H, H}, 64, 16) ||
+        !make_map(&P.ygm, TcMat{s.st_yg, 16, d, d}, 64, 16) || !make_map(&P.ucm, TcMat{s.st_uc, 32, d, d}, 64, 32))
       return TGP_E_CUDA;
-    if (!make_map(&P.ygm, TcMat{s.st_yg, 16, d, d}, 64, 16)) return TGP_E_CUDA;
-    if (!make_map(&P.ucm, TcMat{s.st_uc, 32, d, d}, 64, 32)) return TGP_E_CUDA;
+    P.yg = (__nv_bfloat16*)s.st_yg;
+    P.uc = (__nv_bfloat16*)s.st_uc;
     P.gamma = mparam(s, Ly, 0);
     P.beta = mparam(s, Ly, 1);
     P.b1 = mparam(s, Ly, 3);
@@ -267,8 +263,6 @@ static int st_build_desc(tgp_ctx* c, Stage& s, int B) {
     P.c2fold = P.cfold + 2 * H;
     P.c2part = s.st_c2part + (size_t)(l - s.l0) * (d / 256) * H;
     P.w2 = (const __nv_bfloat16*)w2;
-    P.uc = (__nv_bfloat16*)s.st_uc;
-    P.yg = (__nv_bfloat16*)s.st_yg;
     P.w1 = (const __nv_bfloat16*)w1;
     P.drop_thresh = drop_thresh(Ly.L.dropout);
     P.drop_scale = Ly.L.dropout > 0 ? 1.0f / (1.0f - Ly.L.dropout) : 1.0f;
@@ -339,7 +333,6 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
   t.cnt = s.st_cnt;
   t.seed = c->seed;
   t.step = s.dstep;
-  t.flags = c->st_flags;
   t.sleep_ns = c->st_sleep_ns;
   if (getenv("TGP_ST_DEBUG")) {  // diagnostics: per-CTA, per-phase %globaltimer stamps
     const size_t nd = (size_t)s.st_clusters * 4 * 2 * t.L * ST_DBG_SLOTS;

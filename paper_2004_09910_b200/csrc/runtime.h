@@ -164,10 +164,9 @@ struct tgp_ctx {
   bool use_graphs = true, use_pdl = true, trace = false, poison = false, prefetch = false;
   bool l2pf = false;
   bool stream = true;
-  int st_flags = 0;
   bool gemm_wide = true;      // per-micro-batch GEMMs with >= 256 rows through the persistent gemm_wide kernel (option "gemm_wide")
   bool dw_persistent = true;  // deferred dW through the persistent gemm_dw kernel (option "dw_persistent")
-  unsigned st_sleep_ns = 32;  // stream kernel: back-off between dependency polls (option "stream_poll_ns")  // test only: bit 0 = stream kernel ignores dependencies (timing of the bare weight stream)  // persistent weight-streaming task kernel where eligible (task_stream.cu)
+  unsigned st_sleep_ns = 32;  // stream kernel: back-off between dependency polls (option "stream_poll_ns")
   // Table 1 ablation toggles: 0 / false = the torchgpipe design
   uint64_t order_seed = 0;   // "ablate_order": backward tasks in a seeded random topological order
   bool relay = false;        // "ablate_portals": skip tensors tuple-threaded through every partition

@@ -14,14 +14,10 @@ struct alignas(64) SLayer {
   CUtensorMap w2k;   // W2 [d][H] bf16, K-major box {64, 128}  (forward GEMM2: out d, K H)
   CUtensorMap w2m;   // W2 [d][H] bf16, MN-major box {64, 64}  (backward dG = dY W2: out H, K d)
   CUtensorMap w1m;   // W1 [H][d] bf16, MN-major box {64, 64}  (backward dH = dA W1: out d, K H)
-  CUtensorMap hop;   // Hop  [max_batch][d] bf16, box {64, 16}  (LN output = GEMM1 operand, dW1 stash)
   CUtensorMap gop;   // Gop  [max_batch][H] bf16, box {64, 16}  (activation = GEMM2 operand, dW2 stash)
-  CUtensorMap dyop;  // dYop [max_batch][d] bf16, box {64, 16}  (output grad = dG operand, dW2 stash)
   CUtensorMap daop;  // dAop [max_batch][H] bf16, box {64, 16}  (pre-act grad = dH operand, dW1 stash)
   CUtensorMap ygm;   // yg [16][d] bf16, box {64, 16}: forward GEMM1 operand gamma (y - mu~) (task scratch)
   CUtensorMap ucm;   // uc [32][d] bf16, box {64, 32}: backward dG operand [u | n] (task scratch)
-  CUtensorMap w1c;   // diagnostics: W1 viewed as contiguous 16 KB tiles [H*d/64][64], box {64, 128}
-  CUtensorMap w2c;   // diagnostics: W2 likewise
   const float* gamma;
   const float* beta;
   const float* b1;
@@ -31,9 +27,9 @@ struct alignas(64) SLayer {
   const float* c2fold; // [H] c2_h = sum_k W2[k][h]  (column sums of W2 [d][H])
   float* c2part;       // [d/256][H] stage-1 partial column sums
   __nv_bfloat16* yg;   // [16][d] GEMM1 operand scratch (the memory behind ygm)
+  __nv_bfloat16* uc;   // [32][d] backward dG operand scratch (the memory behind ucm)
   const __nv_bfloat16* w1;  // W1 [H][d] (for the fold kernel)
   const __nv_bfloat16* w2;  // W2 [d][H]
-  __nv_bfloat16* uc;        // [32][d] backward dG operand scratch (the memory behind ucm)
   uint32_t drop_thresh;  // dropout after GELU: keep iff (philox word >> 8) >= thresh (0 = none)
   float drop_scale;
   uint32_t site;         // global layer index (Philox counter word 2)
@@ -64,16 +60,12 @@ struct STask {
                          // before the launch; the last CTA of the task zeroes them again
   uint64_t seed;
   const uint32_t* step;  // device optimizer step (dropout counter word 3)
-  // diagnostics only (nullptr / 0 on the product path): per CTA and phase, %globaltimer stamps
-  // [grid][2L][ST_DBG_SLOTS]; flags (test_stream_variant): bit 0 = ignore dependencies, bit 1 = read
-  // each weight tile as one contiguous 16 KB block, bit 2 = no L2 promotion (host), bit 3 =
-  // evict-normal weight policy, bits 4-9 = L2 prefetch distance in tiles (timing experiments:
-  // bits 0/1 make the results garbage)
+  // diagnostics only (nullptr on the product path): per CTA and phase, %globaltimer stamps
+  // [grid][2L][ST_DBG_SLOTS] (TGP_ST_DEBUG); they do not change any result
   unsigned long long* dbg;
-  int flags;
   unsigned sleep_ns;  // back-off between dependency polls
 };
-constexpr int ST_DBG_SLOTS = 10;
+constexpr int ST_DBG_SLOTS = 12;
 
 int task_stream_smem();
 int task_stream_counter_bytes(int L);

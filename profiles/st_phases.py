@@ -20,9 +20,8 @@ blocks = int(opts.get("blocks", 4))
 bwd = int(opts.get("bwd", 0))
 layers = C.resmlp_stack(blocks, 4096)
 P = Pipeline(layers, chunks=32, devices=[0], balance=[blocks], checkpoint="never", max_batch=512, dtype="bf16", seed=1)
+P.set_option("stream_poll_ns", int(opts.get("poll", 32)))
 P.set_option("graphs", 0)
-if int(opts.get("variant", 0)):
-    P.set_option("test_stream_variant", int(opts["variant"]))
 P.init_params(1)
 X = torch.randn(512, 4096, device="cuda")
 T = torch.randn(512, 4096, device="cuda")
@@ -39,11 +38,11 @@ L.tgp_debug_stream_read(P.h, 0, None, 0, ctypes.byref(n))
 buf = np.zeros(n.value, dtype=np.uint64)
 L.tgp_debug_stream_read(P.h, 0, buf.ctypes.data, n.value, ctypes.byref(n))
 NP = 2 * blocks
-G = n.value // (NP * 10)
-ev = buf.reshape(G, NP, 10).astype(np.int64)
-names = ["B issue", "W first", "W last", "B landed", "MMA done", "TMEM rdy", "partials", "signal", "stats", "sig entry"]
+G = n.value // (NP * 12)
+ev = buf.reshape(G, NP, 12).astype(np.int64)
+names = ["B issue", "W first", "W last", "B landed", "MMA done", "TMEM rdy", "partials", "signal", "stats", "sig entry", "MMA half", "cp last"]
 t0 = ev[:, 0, 1].min()
-print(f"{'bwd' if bwd else 'fwd'} task, {blocks} blocks, {G} CTAs, variant={opts.get('variant', 0)}")
+print(f"{'bwd' if bwd else 'fwd'} task, {blocks} blocks, {G} CTAs, ")
 prev = None
 for p in range(NP):
     base = np.median(ev[:, p, 1])

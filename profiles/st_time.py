@@ -1,5 +1,5 @@
-"""F-task time of the stream kernel (no debug stamps) under test_stream_variant values.
-    python profiles/st_time.py v1 v2 ...   (bits: 1 nodep, 2 contiguous tiles, 1024 no MMA, 2048 no TMEM staging)"""
+"""F-task time of the stream kernel (no debug stamps) at dependency-poll back-offs (ns).
+    python profiles/st_time.py [poll_ns ...]"""
 import os
 import sys
 
@@ -12,12 +12,8 @@ from synth import configs as C  # noqa: E402
 P = Pipeline(C.resmlp_stack(32, 4096), chunks=32, devices=[0], balance=[32], checkpoint="except_last", max_batch=512,
              dtype="bf16", seed=1)
 P.init_params(1)
-for a in sys.argv[1:] or ["0"]:
-    v, _, poll = a.partition(":")
-    v = int(v)
-    if poll:
-        P.set_option("stream_poll_ns", int(poll))
-    P.set_option("test_stream_variant", v)
+for a in sys.argv[1:] or ["32"]:
+    P.set_option("stream_poll_ns", int(a))
     P.bench_dominant_gemm(0, 512, reps=2)
     ms, by, n = P.bench_dominant_gemm(0, 512, reps=10)
-    print(f"variant {a:>9s}: F task {ms * 1e3:7.1f} us = {ms * 1e3 / 64:5.2f} us/phase, {by / ms / 1e6:6.0f} GB/s")
+    print(f"poll {a:>6s} ns: F task {ms * 1e3:7.1f} us = {ms * 1e3 / 64:5.2f} us/phase, {by / ms / 1e6:6.0f} GB/s")
