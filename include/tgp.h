@@ -35,7 +35,13 @@ typedef enum {
   TGP_E_CUDA = -3,        /* a CUDA runtime / driver call failed                      */
   TGP_E_NOMEM = -4,       /* device allocation failed                                 */
   TGP_E_UNSUPPORTED = -5, /* shape / device / feature not supported by this build     */
-  TGP_E_TIMEOUT = -6      /* a cross-partition handshake did not complete in time     */
+  TGP_E_TIMEOUT = -6      /* a cross-partition handshake did not complete in time (the
+                             watchdog, option "watchdog_ms"): the call returns instead of
+                             hanging; the context is failed (results garbage; every later
+                             call except tgp_destroy / introspection -> TGP_E_STATE).  The
+                             local receive flags are released to drain the device; if it
+                             does not drain within 2 s, tgp_destroy leaks the device memory
+                             to process exit rather than block                           */
 } tgp_status;
 
 /* Checkpoint policy (P:105, P:108, P:305 footnote; SURVEY reading Z4):
@@ -229,6 +235,13 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *             (default 1; 0 = the one-tile-per-CTA GEMM)
  *  "attn_tc"  PROCESS-WIDE: 1 = tcgen05 attention forward where seq % 128 == 0, 0 = mma.sync,
  *             -1 = the TGP_ATTN_TC environment default (off)
+ *  "watchdog_ms" bound on the host wait for a call's device work (forward / backward), ms
+ *             (default 60000; 0 = unbounded): past it the call returns TGP_E_TIMEOUT (PAPER.md P:133,
+ *             host issue with device-side waits: a lost message would otherwise hang the caller)
+ *  "transport" stage-boundary messages (COPY_F / COPY_B): 0 = SM push kernel
+ *             writing the consumer's receive slab + system-scope release store of the flag (default),
+ *             1 = copy engine (cudaMemcpyAsync peer/D2D) + cuStreamWriteValue32 of the flag.  Skip
+ *             tensors always use the push kernel (bf16 conversion).  Same bytes either way.
  * Table 1 ablation toggles (results are bitwise those of the default -- only the
  * issue order and the copy path change).  Need every partition in this process, and not between
  * forward and backward (TGP_E_UNSUPPORTED / TGP_E_STATE):
@@ -241,7 +254,8 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  * Test-only negative controls (never used on the product path):
  *  "test_poison"        fill the forward receive slabs with NaN before each forward call
  *  "test_skip_wait"     drop the receive waits of partition `value` (-1 = none)
- *  "test_delay_push_us" delay every push on its copy stream by `value` microseconds */
+ *  "test_delay_push_us" delay every push on its copy stream by `value` microseconds
+ *  "test_drop_push"     partition `value` never sends its forward messages (watchdog test; -1 = off) */
 tgp_status tgp_set_option(tgp_ctx* ctx, const char* name, int64_t value);
 
 const char* tgp_last_error(void);
@@ -270,6 +284,16 @@ tgp_status tgp_memory(tgp_ctx* ctx, int32_t part, int64_t* used, int64_t* reserv
  * `reps`, measured with CUDA events between the layers on the per-layer kernel path.
  * ms_per_layer: host array of the partition's layer count.  Feed it to tgp_balance. */
 tgp_status tgp_profile_layers(tgp_ctx* ctx, int32_t part, int32_t B, int32_t reps, double* ms_per_layer);
+
+/* Transport micro-benchmark (PAPER.md P:198-203 copy streams): messages of
+ * `bytes` (multiple of 16) fp32 from a device buffer on dev_src to a receive buffer on dev_dst
+ * (dev_src == dev_dst allowed; peer access is enabled for different devices) through the pipeline's
+ * transports: mode 0 = SM push kernel + release flag, mode 1 = copy engine + stream-written flag.
+ * *us_stream: device µs per message of `reps` back-to-back messages, each waited for by a consumer
+ * stream; *us_pingpong: µs per message + acknowledgement round trip.  Buffers are allocated and freed
+ * here.  TGP_E_UNSUPPORTED without peer access, TGP_E_INVALID for bad sizes. */
+tgp_status tgp_bench_transport(int32_t dev_src, int32_t dev_dst, int64_t bytes, int32_t mode, int32_t reps,
+                               double* us_stream, double* us_pingpong);
 
 /* *on = 1 iff local partition `part` runs its F / F' / B tasks as the persistent weight-streaming
  * task kernel (eligible shape and option "stream" on); then tgp_bench_dominant_gemm times that

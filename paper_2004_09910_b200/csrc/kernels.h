@@ -110,6 +110,7 @@ int push_bytes(cudaStream_t st, const void* src, void* dst, int64_t nbytes, uint
                uint32_t seq);
 // Release-store value into *flag (system scope) from a 1-thread kernel.
 int signal_flag(cudaStream_t st, uint32_t* flag, uint32_t value);
+int fill_flags(cudaStream_t st, uint32_t* p, int64_t n, uint32_t v);
 // Test-only: busy a stream for ns nanoseconds.
 int spin(cudaStream_t st, uint64_t ns);
 

@@ -422,14 +422,22 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ uint32_t atom_add_acq_rel_sys(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// The CTA's stores are ordered before thread 0's release-add by the barrier (release is cumulative);
+// the last CTA's acquire-add reads the chain of every CTA's release, so its release store of the flag
+// publishes the whole message at system scope (peer GPUs, CUDA-IPC mappings).  Single CTA: no counter.
 __device__ __forceinline__ void finish_push(uint32_t* counter, uint32_t* flag, uint32_t seq) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    const uint32_t prev = atomicAdd(counter, 1u);
-    if (prev == gridDim.x - 1) {
-      *counter = 0u;
-      __threadfence_system();
+    if (gridDim.x == 1) {
+      st_release_sys(flag, seq);
+    } else if (atom_add_acq_rel_sys(counter, 1u) == gridDim.x - 1) {
+      *counter = 0u;  // reset for the next push on this stream (ordered before it by the stream)
       st_release_sys(flag, seq);
     }
   }
@@ -496,9 +504,15 @@ __global__ void spin_kernel(uint64_t ns) {
 }
 int spin(cudaStream_t st, uint64_t ns) { return launch("spin", spin_kernel, dim3(1), dim3(1), st, false, ns); }
 
-__global__ void signal_kernel(uint32_t* flag, uint32_t v) {
-  __threadfence_system();
-  st_release_sys(flag, v);
+__global__ void signal_kernel(uint32_t* flag, uint32_t v) { st_release_sys(flag, v); }
+
+// watchdog release: every flag a stream may wait on is set far ahead of any sequence number
+__global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    st_release_sys(p + i, v);
+}
+int fill_flags(cudaStream_t st, uint32_t* p, int64_t n, uint32_t v) {
+  return launch("fill_flags", fill_u32_kernel, dim3(1), dim3(256), st, false, p, n, v);
 }
 int signal_flag(cudaStream_t st, uint32_t* flag, uint32_t value) {
   return launch("signal", signal_kernel, dim3(1), dim3(1), st, false, flag, value);

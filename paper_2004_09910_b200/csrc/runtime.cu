@@ -6,11 +6,13 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 
 #include "host.h"
 #include "runtime.h"
@@ -873,6 +875,13 @@ static int wait_flag(tgp_ctx* c, cudaStream_t st, uint32_t* flag, uint32_t v) {
   return 0;
 }
 
+static int write_flag(cudaStream_t st, uint32_t* flag, uint32_t v) {
+  const Driver* d = driver();
+  if (!d) return TGP_E_CUDA;
+  TGP_CU_TRY(d->streamWriteValue32((CUstream)st, (CUdeviceptr)flag, v, CU_STREAM_WRITE_VALUE_DEFAULT));
+  return 0;
+}
+
 static void trace_begin(tgp_ctx* c, Stage& s, cudaStream_t st, int stream_id, int kind, int i, cudaEvent_t* a) {
   if (!c->trace) return;
   cudaEventCreate(a);
@@ -969,6 +978,7 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
         first_push[src][dst] = 1;
       }
       const ArenaView& pv = c->view[dst];
+      if (c->drop_push_part == src && rc.kind == K_COPY_F) return 0;  // watchdog test: the message is lost
       if (c->delay_push_ns) {  // negative-control tests: make a missing receive wait observable
         TGP_TRY(spin(st, c->delay_push_ns));
         c->kernels++;
@@ -977,7 +987,17 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       trace_begin(c, s, st, skip ? 2 : 1, rc.kind, i, &ta);
       uint32_t* ctr = s.counters + (skip ? 1 : 0);
       int64_t nbytes = 0;
-      if (rc.kind == K_COPY_F) {
+      if ((rc.kind == K_COPY_F || rc.kind == K_COPY_B) && c->transport == 1) {
+        // copy-engine transport: DMA copy, then a stream memory write of the flag (the driver orders it
+        // after the copy with a memory barrier: CU_STREAM_WRITE_VALUE_DEFAULT)
+        const bool fw = rc.kind == K_COPY_F;
+        const int w = fw ? s.d_out : s.d_in;
+        nbytes = (int64_t)M * w * 4;
+        const float* from = (fw ? s.out : s.dx_out) + (size_t)r0 * w;
+        float* to = (fw ? pv.fwd_in : pv.grad_in) + (size_t)r0 * w;
+        TGP_CUDA_TRY(cudaMemcpyAsync(to, from, (size_t)nbytes, cudaMemcpyDefault, st));
+        TGP_TRY(write_flag(st, fw ? flag_fwd(pv, i) : flag_grad(c, pv, i), seq));
+      } else if (rc.kind == K_COPY_F) {
         nbytes = (int64_t)M * s.d_out * 4;
         TGP_TRY(push_rows(st, s.out + (size_t)r0 * s.d_out, pv.fwd_in + (size_t)r0 * s.d_out, false,
                           (int64_t)M * s.d_out, ctr, flag_fwd(pv, i), seq));
@@ -1078,6 +1098,69 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
   return 0;
 }
 
+// Bounded host wait for every local stream of the call ("a handshake wait past the
+// watchdog -> TGP_E_TIMEOUT"; the host issues, the device waits).  A lost message or
+// flag leaves a consumer stream in cuStreamWaitValue32 forever; past `watchdog_ms` the call returns
+// TGP_E_TIMEOUT instead of hanging.  It first tries to release every local receive flag far ahead of
+// any sequence number from a fresh stream and to drain the device (bounded); the context is failed
+// either way (the call's results are garbage).  Measured on B200: while a stream-memory wait is
+// pending the release kernel may not get to run (profiles/diag/wd_dbg.py), so when the device does
+// not drain the context is also marked wedged: tgp_destroy then skips every CUDA call that could
+// block and leaks the device memory to process exit, where the driver reclaims it.
+static bool streams_idle(tgp_ctx* c) {
+  for (Stage* q : c->local) {
+    if (!q) continue;
+    cudaSetDevice(q->dev);
+    for (cudaStream_t st : {q->comp, q->cact, q->cskip})
+      if (cudaStreamQuery(st) == cudaErrorNotReady) return false;
+  }
+  return true;
+}
+
+static int sync_with_watchdog(tgp_ctx* c) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto ms_since = [](std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+  };
+  for (int j = 0; j < c->n; ++j) {
+    Stage* sp = c->local[j];
+    if (!sp) continue;
+    TGP_CUDA_TRY(cudaSetDevice(sp->dev));
+    for (cudaStream_t st : {sp->comp, sp->cact, sp->cskip}) {
+      while (true) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e == cudaSuccess) break;
+        if (e != cudaErrorNotReady) {
+          set_error("CUDA error: %s", cudaGetErrorString(e));
+          return TGP_E_CUDA;
+        }
+        if (c->watchdog_ms > 0 && ms_since(t0) > (double)c->watchdog_ms) {
+          for (Stage* q : c->local) {
+            if (!q) continue;
+            cudaSetDevice(q->dev);
+            cudaStream_t rs = nullptr;
+            if (cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking) == cudaSuccess)
+              fill_flags(rs, q->self.flags, n_flags(c), c->seq + 0x40000000u);  // stream leaked if wedged
+          }
+          const auto t1 = std::chrono::steady_clock::now();
+          bool idle = false;
+          while (!(idle = streams_idle(c)) && ms_since(t1) < 2000.0)
+            std::this_thread::sleep_for(std::chrono::microseconds(100));
+          c->failed = true;
+          c->wedged = !idle;
+          set_error("watchdog: partition %d (device %d) did not complete the call within %lld ms (a lost message or "
+                    "flag); %s -- destroy the context",
+                    j, sp->dev, (long long)c->watchdog_ms,
+                    idle ? "waits released, device drained" : "device did not drain (resources leak to process exit)");
+          return TGP_E_TIMEOUT;
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
+    }
+  }
+  return 0;
+}
+
 static int finish_call(tgp_ctx* c) {
   // tell every partition that writes into a local partition that this call is done on it
   for (int j = 0; j < c->n; ++j) {
@@ -1088,14 +1171,7 @@ static int finish_call(tgp_ctx* c) {
       c->kernels++;
     }
   }
-  for (int j = 0; j < c->n; ++j) {
-    Stage* sp = c->local[j];
-    if (!sp) continue;
-    TGP_CUDA_TRY(cudaSetDevice(sp->dev));
-    TGP_CUDA_TRY(cudaStreamSynchronize(sp->comp));
-    TGP_CUDA_TRY(cudaStreamSynchronize(sp->cact));
-    TGP_CUDA_TRY(cudaStreamSynchronize(sp->cskip));
-  }
+  TGP_TRY(sync_with_watchdog(c));
   if (c->trace) {
     for (auto& t : c->trace_recs) {
       Stage* s = c->local[t.part];

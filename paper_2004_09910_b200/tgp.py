@@ -22,7 +22,11 @@ F, RECOMPUTE, B, COPY_F, COPY_B, SKIP_F, SKIP_B, W = range(8)
 
 
 class TgpError(RuntimeError):
-    pass
+    """A tgp_* call returned a status != 0 (`rc`, include/tgp.h tgp_status)."""
+
+    def __init__(self, msg, rc=None):
+        super().__init__(msg)
+        self.rc = rc
 
 
 class Layer(ctypes.Structure):
@@ -76,6 +80,8 @@ _SIGS = {
     "tgp_profile_layers": [_P, _I32, _I32, _I32, ctypes.POINTER(ctypes.c_double)],
     "tgp_memory": [_P, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
     "tgp_test_gemm_bf16": [_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P],
+    "tgp_bench_transport": [_I32, _I32, _I64, _I32, _I32, ctypes.POINTER(ctypes.c_double),
+                            ctypes.POINTER(ctypes.c_double)],
 }
 
 
@@ -101,7 +107,7 @@ def exported_symbols():
 def _check(rc, what):
     if rc != 0:
         msg = lib().tgp_last_error()
-        raise TgpError(f"{what} failed ({rc}): {msg.decode() if msg else ''}")
+        raise TgpError(f"{what} failed ({rc}): {msg.decode() if msg else ''}", rc)
 
 
 def _ptr(t):
@@ -329,6 +335,15 @@ class Pipeline:
 
     def set_option(self, name, value):
         _check(lib().tgp_set_option(self.h, name.encode(), int(value)), "tgp_set_option")
+
+
+def bench_transport(dev_src, dev_dst, nbytes, mode=0, reps=50):
+    """Per-message device time of the stage-boundary transport (tgp_bench_transport): mode 0 = SM push
+    kernel + release flag, 1 = copy engine + stream-written flag.  Returns (us_stream, us_pingpong)."""
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _check(lib().tgp_bench_transport(dev_src, dev_dst, int(nbytes), mode, reps, ctypes.byref(a), ctypes.byref(b)),
+           "tgp_bench_transport")
+    return a.value, b.value
 
 
 def balance_by_time(layers, n_parts, *, batch, chunks, device=0, dtype="bf16", reps=5, seed=0):
