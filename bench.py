@@ -122,41 +122,63 @@ def _dist():
     return ws, rank, lrank
 
 
-def cpu_oracle_sample(steps=1, blocks=8, batch=BATCH, width=WIDTH):
-    """Time the fp64 oracle (as it stands) on a bounded sample of C2: `blocks` of the 32 blocks at full
-    width and full batch; returns (samples/s scaled to the full 32-block model, cores, description)."""
+def _host_info():
+    """CPU model, BLAS implementation / version and its thread count (threadpoolctl)."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas, threads = None, os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_info
+        info = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if info:
+            blas = f"{info[0].get('internal_api')} {info[0].get('version')}"
+            threads = max(int(i.get("num_threads", 0)) for i in info)
+    except Exception:
+        pass
+    return model, blas, threads
+
+
+def cpu_oracle_sample(steps=3, batch=64, width=WIDTH):
+    """Time the fp64 oracle (as it stands) on a bounded sample of C2: the FULL 32-block model at full
+    width on `batch` of the 512 rows (the oracle is full-batch: its cost is linear in the rows, so
+    samples/s does not depend on the sample size).  Median of `steps` timed steps after one untimed.
+    Returns (samples/s, threads, description, median step seconds)."""
     from oracle import model as OM
     from synth import configs as C
     from synth import gen as G
 
-    layers = C.resmlp_stack(blocks, width)
+    layers = C.resmlp_stack(BLOCKS, width)
     x, t = G.inputs(layers, batch, seed=1234, dtype="bf16")
     params = G.params(layers, seed=1234, dtype="bf16")
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([int(i.get("num_threads", 0)) for i in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
+    model, blas, threads = _host_info()
+    OM.train_step(layers, params, x, t, lr=0.05, m=M_CHUNKS, want_dx=False)
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
         OM.train_step(layers, params, x, t, lr=0.05, m=M_CHUNKS, want_dx=False)
         times.append(time.perf_counter() - t0)
-    per_step = statistics.median(times) * (BLOCKS / blocks)
-    desc = (f"oracle.model.train_step (numpy fp64) on {blocks} of the {BLOCKS} RESMLP blocks at width {width}, "
-            f"batch {batch}; median of {steps} step(s) scaled x{BLOCKS // blocks} to the full model")
-    return batch / per_step, cores, desc
+    per_step = statistics.median(times)
+    desc = (f"oracle.model.train_step (numpy fp64), the full {BLOCKS}-block model at width {width} on {batch} of the "
+            f"{BATCH} rows (m={M_CHUNKS}); median of {steps} steps ({per_step:.2f} s each) after one untimed; "
+            f"CPU: {model}; BLAS: {blas}, {threads} threads")
+    return batch / per_step, threads, desc, per_step
 
 
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    # each step a bounded sample (2 of the 32 blocks at full width and batch, ~7 s on 16 cores) so a
-    # --steps K run of the reference arm stays within a few minutes
-    v, cores, desc = cpu_oracle_sample(steps=max(1, args.steps), blocks=min(args.ref_blocks, 2))
+    # each step = the full 32-block model on a bounded sample of the batch (64 of 512 rows, ~2 s on 16
+    # cores): ms_per_step is what was timed, so a --steps K run of this arm fits its wall time
+    v, cores, desc, per_step = cpu_oracle_sample(steps=max(1, args.steps), batch=args.ref_rows)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH / v,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config(args.gpus),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
@@ -193,7 +215,8 @@ def run_tgp(args):
     devices = [-1] * n
     devices[rank] = lrank
     free0 = torch.cuda.mem_get_info(dev)[0]
-    P = Pipeline(layers, chunks=args.chunks, devices=devices, balance=[BLOCKS // n] * n, checkpoint=args.checkpoint,
+    bal = [BLOCKS // n + (1 if j < BLOCKS % n else 0) for j in range(n)]
+    P = Pipeline(layers, chunks=args.chunks, devices=devices, balance=bal, checkpoint=args.checkpoint,
                  max_batch=BATCH, dtype="bf16", seed=1234)
     if ws > 1:
         from paper_2004_09910_b200.dist import connect_pipeline
@@ -234,34 +257,57 @@ def run_tgp(args):
 
     def timed(k, e2e, clk=None):
         barrier()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(k + 1)]
         k0 = P.kernel_count()
         if clk:
             clk.begin()
-        a.record()
-        losses = [step(e2e) for _ in range(k)]
-        b.record()
-        b.synchronize()
+        ev[0].record()
+        losses = []
+        for q in range(k):
+            losses.append(step(e2e))
+            ev[q + 1].record()
+        ev[k].synchronize()
         if clk:
             clk.end()
-        ms = a.elapsed_time(b)
+        ms = ev[0].elapsed_time(ev[k])
+        per = [ev[q].elapsed_time(ev[q + 1]) for q in range(k)]
         nk = P.kernel_count() - k0
         barrier()
         if ws > 1:
             from paper_2004_09910_b200.dist import max_over_ranks
             ms = max_over_ranks(ms)
-        return ms, nk, losses
+            per = [max_over_ranks(v) for v in per]
+        return ms, nk, losses, per
 
     for _ in range(args.warmup):
         step()
     clk = ClockSampler(lrank)
     clk.start()
     free_t0 = torch.cuda.mem_get_info(dev)[0]
-    ms, nk, losses = timed(args.steps, False, clk)
+    ms, nk, losses, per_step = timed(args.steps, False, clk)
     free_t1 = torch.cuda.mem_get_info(dev)[0]
     clocks = clk.stop()
-    e2e_ms, _, _ = timed(args.steps, True)
+    e2e_ms, _, _, _ = timed(args.steps, True)
+
+    # one traced step (after the timed ones): per-task device intervals -> busy / bubble fraction of
+    # this partition's compute stream (busy_j against m / (m + n - 1)) and task times
+    P.set_trace(True)
+    barrier()
+    P.forward(X, BATCH, Y)
+    if last:
+        P.mse_loss_grad(Y, T, BATCH, DY)
+    P.backward(DY, None)
+    tl = P.timeline()
+    P.set_trace(False)
+    P.step(args.lr)
+    comp = tl[(tl[:, 0] == rank) & (tl[:, 1] == 0)]
+    kinds = {0: "F", 1: "F'", 2: "B", 7: "W"}
+    task_us = {}
+    for kd, nm in kinds.items():
+        d = (comp[comp[:, 2] == kd][:, 5] - comp[comp[:, 2] == kd][:, 4]) / 1e3
+        if len(d):
+            task_us[nm] = {"n": int(len(d)), "median_us": float(np.median(d)), "sum_ms": float(d.sum() / 1e3)}
+    busy_ms = float((comp[:, 5] - comp[:, 4]).sum() / 1e6)
 
     # dominant kernel: forward weight-streaming GEMM, timed live on its stream (cycling cold weights)
     # dominant kernel: the persistent weight-streaming task kernel (F task of micro-batch 1: 2 GEMMs
@@ -287,13 +333,36 @@ def run_tgp(args):
             traffic = None
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        v, cores, desc = cpu_oracle_sample(steps=1, blocks=args.ref_blocks)
+        v, cores, desc, _ = cpu_oracle_sample(steps=3, batch=args.cpu_rows)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+    # per GEMM class, three fractions: achieved TFLOP/s / bf16 peak, achieved DRAM GB/s /
+    # HBM peak, and achieved / the class's own roofline min(TC peak, AI x HBM)
+    tc_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1385.9))) if peaks else 1385.9
+    nb, d_, m_ = BLOCKS // n, WIDTH, BATCH // args.chunks
+
+    def fractions(flop, dram_bytes, sec):
+        tf, gbs = flop / sec / 1e12, dram_bytes / sec / 1e9
+        roof = min(tc_peak, (flop / dram_bytes) * peak / 1e3)  # TFLOP/s
+        return {"tflops": tf, "frac_tc": tf / tc_peak, "dram_gbs": gbs, "frac_hbm": gbs / peak,
+                "frac_own_roofline": tf / roof}
+    gemm_fr = {}
+    if stream:
+        gemm_fr["stream_F_task"] = fractions(nb * 2 * 2.0 * m_ * d_ * d_, gemm_bytes, gemm_ms * 1e-3)
+    if "W" in task_us:  # deferred dW: 2 GEMMs per block of 4096 x 4096 x B, bf16 operands, fp32 dW out
+        wflop = nb * 2 * 2.0 * d_ * d_ * BATCH
+        wbytes = nb * 2 * (2.0 * BATCH * d_ * 2 + 4.0 * d_ * d_)
+        gemm_fr["wgrad_task"] = fractions(wflop, wbytes, task_us["W"]["median_us"] * 1e-6)
     if rank == 0:
         sps = BATCH * args.steps / (ms * 1e-3)
         line = {
             "metric": METRIC, "value": sps, "unit": UNIT, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "step_ms": {"p10": float(np.percentile(per_step, 10)), "p50": float(np.percentile(per_step, 50)),
+                        "p90": float(np.percentile(per_step, 90))},
+            "pipeline": {"busy": busy_ms / (ms / args.steps), "bubble": 1.0 - busy_ms / (ms / args.steps),
+                         "ideal_busy": args.chunks / (args.chunks + n - 1), "tasks": task_us,
+                         "note": "busy = sum of this rank's compute-task intervals in one traced step / ms_per_step"},
+            "gemm_fractions": gemm_fr,
             "dtype": "bf16", "data": "synthetic (N(0,1) inputs/targets, on-device U(+-1/sqrt(fan_in)) init)",
             "config": _config(n, args.chunks, args.checkpoint),
             "e2e": {"value": BATCH * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
@@ -328,7 +397,8 @@ def main():
     ap.add_argument("--checkpoint", default="except_last", choices=["always", "except_last", "never"])
     ap.add_argument("--chunks", type=int, default=M_CHUNKS, help="m (BASELINE metric: 32; other values = C3 sweep)")
     ap.add_argument("--lr", type=float, default=0.05)
-    ap.add_argument("--ref-blocks", type=int, default=4)
+    ap.add_argument("--ref-rows", type=int, default=64, help="reference arm: rows of the full-model oracle sample")
+    ap.add_argument("--cpu-rows", type=int, default=128, help="cpu_baseline: rows of the full-model oracle sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--opt", action="append", default=[], help="runtime option name=value (tgp_set_option)")
     args = ap.parse_args()

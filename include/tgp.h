@@ -239,9 +239,11 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *             (default 60000; 0 = unbounded): past it the call returns TGP_E_TIMEOUT (PAPER.md P:133,
  *             host issue with device-side waits: a lost message would otherwise hang the caller)
  *  "transport" stage-boundary messages (COPY_F / COPY_B): 0 = SM push kernel
- *             writing the consumer's receive slab + system-scope release store of the flag (default),
- *             1 = copy engine (cudaMemcpyAsync peer/D2D) + cuStreamWriteValue32 of the flag.  Skip
- *             tensors always use the push kernel (bf16 conversion).  Same bytes either way.
+ *             writing the consumer's receive slab + system-scope release store of the flag,
+ *             1 = copy engine (cudaMemcpyAsync peer/D2D) + cuStreamWriteValue32 of the flag,
+ *             2 = by message size: copy engine from 16 KiB up (the B200 crossover of
+ *             tgp_bench_transport; default).  Skip tensors always use the push kernel (bf16
+ *             conversion).  Same bytes either way: results are bitwise identical.
  * Table 1 ablation toggles (results are bitwise those of the default -- only the
  * issue order and the copy path change).  Need every partition in this process, and not between
  * forward and backward (TGP_E_UNSUPPORTED / TGP_E_STATE):
@@ -297,8 +299,9 @@ tgp_status tgp_bench_transport(int32_t dev_src, int32_t dev_dst, int64_t bytes, 
 
 /* *on = 1 iff local partition `part` runs its F / F' / B tasks as the persistent weight-streaming
  * task kernel (eligible shape and option "stream" on); then tgp_bench_dominant_gemm times that
- * kernel (F_{1,j} launches: *bytes = its algorithmic bytes -- weights plus activations read and
- * written once) instead of the per-layer forward GEMM. */
+ * kernel (F_{1,j} launches: *bytes = its algorithmic bytes per SURVEY 8(d) -- the bf16 weights of
+ * every block once plus the fp32 stage input read and stage output written; intermediates are not
+ * counted) instead of the per-layer forward GEMM. */
 tgp_status tgp_stream_enabled(tgp_ctx* ctx, int32_t part, int32_t* on);
 
 /* Diagnostics of the persistent weight-streaming task kernel (only when the process runs with

@@ -875,6 +875,11 @@ static int wait_flag(tgp_ctx* c, cudaStream_t st, uint32_t* flag, uint32_t v) {
   return 0;
 }
 
+// transport "auto" (2): copy engine from this message size up, SM push kernel below -- the crossover
+// measured on B200 (profiles/round2_transport_sweep.txt: push 4.7 us vs CE 5.7 us at 4 KiB, CE 6.2 us
+// vs push 7.3 us at 16 KiB and flat to 4 MiB)
+constexpr int64_t kCeMinBytes = 16384;
+
 static int write_flag(cudaStream_t st, uint32_t* flag, uint32_t v) {
   const Driver* d = driver();
   if (!d) return TGP_E_CUDA;
@@ -987,7 +992,9 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       trace_begin(c, s, st, skip ? 2 : 1, rc.kind, i, &ta);
       uint32_t* ctr = s.counters + (skip ? 1 : 0);
       int64_t nbytes = 0;
-      if ((rc.kind == K_COPY_F || rc.kind == K_COPY_B) && c->transport == 1) {
+      const int64_t msg_bytes = (int64_t)M * (rc.kind == K_COPY_F ? s.d_out : s.d_in) * 4;
+      const bool use_ce = c->transport == 1 || (c->transport == 2 && msg_bytes >= kCeMinBytes);
+      if ((rc.kind == K_COPY_F || rc.kind == K_COPY_B) && use_ce) {
         // copy-engine transport: DMA copy, then a stream memory write of the flag (the driver orders it
         // after the copy with a memory barrier: CU_STREAM_WRITE_VALUE_DEFAULT)
         const bool fw = rc.kind == K_COPY_F;

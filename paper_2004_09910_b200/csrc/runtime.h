@@ -175,7 +175,7 @@ struct tgp_ctx {
   int splitk = 0, skip_wait_part = -1;
   uint64_t delay_push_ns = 0;
   int drop_push_part = -1;    // test only: partition whose forward messages are never sent (watchdog test)
-  int transport = 0;          // 0 = SM push kernel + release flag, 1 = copy engine + stream write (option "transport")
+  int transport = 2;          // 0 = SM push kernel + release flag, 1 = copy engine + stream write, 2 = auto by size (option "transport")
   int64_t watchdog_ms = 60000;  // bound on a call's device wait (option "watchdog_ms"); 0 = wait forever
   bool failed = false;        // a watchdog timeout left the context unusable (every call: TGP_E_STATE)
   bool wedged = false;        // ... and the device did not drain: destroy must not block (leaks)
