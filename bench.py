@@ -11,8 +11,9 @@ paper's default, P:108 / P:305 fn), bf16 operands with fp32 accumulation, plain 
 synthetic N(0,1) data.  N GPUs = N partitions of 32/N blocks (one process per GPU, partitions
 connected through CUDA-IPC receive arenas); total work fixed -> "scaling": "strong".
 
-A step = tgp_forward + tgp_mse_loss_grad + tgp_backward + tgp_step (all GPipe tasks: F, F', B, W,
-copies, SGD).  `value` is timed with CUDA events on the device with inputs resident in HBM;
+A step = tgp_forward + tgp_mse_loss_grad + tgp_backward_step (all GPipe tasks: F, F', B, W with the
+SGD update fused into it, copies; --unfused-sgd: tgp_backward + tgp_step).  `value` is timed with
+CUDA events on the device with inputs resident in HBM;
 `e2e` additionally copies x / target host->device (pinned) every step and reads the loss back.
 The 2.15 GB of bf16 weights streamed per step exceed the 126 MB L2, so no explicit L2 flush.
 `--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample of the same workload.
@@ -245,8 +246,11 @@ def run_tgp(args):
             torch.cuda.current_stream().synchronize()
         P.forward(X, BATCH, Y)
         loss = P.mse_loss_grad(Y, T, BATCH, DY) if last else None  # loss is read back to the host
-        P.backward(DY, None)
-        P.step(args.lr)
+        if args.unfused_sgd:
+            P.backward(DY, None)
+            P.step(args.lr)
+        else:
+            P.backward_step(DY, args.lr)
         return loss
 
     def barrier():
@@ -296,10 +300,14 @@ def run_tgp(args):
     P.forward(X, BATCH, Y)
     if last:
         P.mse_loss_grad(Y, T, BATCH, DY)
-    P.backward(DY, None)
+    if args.unfused_sgd:
+        P.backward(DY, None)
+    else:
+        P.backward_step(DY, args.lr)
     tl = P.timeline()
     P.set_trace(False)
-    P.step(args.lr)
+    if args.unfused_sgd:
+        P.step(args.lr)
     comp = tl[(tl[:, 0] == rank) & (tl[:, 1] == 0)]
     kinds = {0: "F", 1: "F'", 2: "B", 7: "W"}
     task_us = {}
@@ -348,10 +356,13 @@ def run_tgp(args):
     gemm_fr = {}
     if stream:
         gemm_fr["stream_F_task"] = fractions(nb * 2 * 2.0 * m_ * d_ * d_, gemm_bytes, gemm_ms * 1e-3)
-    if "W" in task_us:  # deferred dW: 2 GEMMs per block of 4096 x 4096 x B, bf16 operands, fp32 dW out
+    if "W" in task_us:
+        # deferred dW: 2 GEMMs per block of 4096 x 4096 x B, bf16 operands; unfused: fp32 dW out;
+        # fused with SGD: fp32 master read + write and bf16 shadow write (10 B/param), no dW out
         wflop = nb * 2 * 2.0 * d_ * d_ * BATCH
-        wbytes = nb * 2 * (2.0 * BATCH * d_ * 2 + 4.0 * d_ * d_)
-        gemm_fr["wgrad_task"] = fractions(wflop, wbytes, task_us["W"]["median_us"] * 1e-6)
+        wbytes = nb * 2 * (2.0 * BATCH * d_ * 2 + (4.0 if args.unfused_sgd else 10.0) * d_ * d_)
+        gemm_fr["wgrad_task" if args.unfused_sgd else "wgrad_sgd_task"] = fractions(wflop, wbytes,
+                                                                                   task_us["W"]["median_us"] * 1e-6)
     if rank == 0:
         sps = BATCH * args.steps / (ms * 1e-3)
         line = {
@@ -400,6 +411,7 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=64, help="reference arm: rows of the full-model oracle sample")
     ap.add_argument("--cpu-rows", type=int, default=128, help="cpu_baseline: rows of the full-model oracle sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--unfused-sgd", action="store_true", help="tgp_backward + tgp_step instead of tgp_backward_step")
     ap.add_argument("--opt", action="append", default=[], help="runtime option name=value (tgp_set_option)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -192,6 +192,15 @@ tgp_status tgp_backward(tgp_ctx* ctx, const float* dy, float* dx);
  * then gradients are logically reset.  Advances the dropout step counter. */
 tgp_status tgp_step(tgp_ctx* ctx, float lr);
 
+/* tgp_backward followed by tgp_step(lr), with the SGD update fused into the deferred weight-gradient
+ * task W_j (g^j = sum_i g_i^j; plain SGD).  In bf16 mode the W1 / W2
+ * matrices of RESMLP blocks (d, H multiples of 128) are updated straight from the dW accumulator
+ * (theta <- theta - lr g with the same fp32 fma as tgp_step, so results are bitwise identical to
+ * tgp_backward + tgp_step); their gradients are NOT stored (tgp_get_grad returns stale values for
+ * them).  Every other parameter, and fp32 mode, takes the unfused path.  Arguments as tgp_backward.
+ * TGP_E_STATE if gradients of an earlier tgp_backward are still pending (call tgp_step first). */
+tgp_status tgp_backward_step(tgp_ctx* ctx, const float* dy, float* dx, float lr);
+
 /* ------------------------------------------------------------------ parameters / introspection */
 
 /* Parameters in canonical order over ALL layers (see tgp_kind).  Only parameters of local
@@ -231,6 +240,8 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *             weight-streaming kernel per task (task_stream.cu; default 1 where eligible)
  *  "dw_persistent" deferred weight gradients through the persistent 128x128-tile dW kernel (default 1)
  *  "stream_poll_ns" back-off of the stream kernel's dependency polling loops, ns (default 32)
+ *  "stream_inflight" max weight tiles (16 KB) a stream-kernel CTA keeps in flight from HBM
+ *                   (0 = as many as its ring has free stages; values >= the ring depth are ignored)
  *  "gemm_wide" per-micro-batch GEMMs with >= 256 rows through the persistent gemm_wide kernel
  *             (default 1; 0 = the one-tile-per-CTA GEMM)
  *  "attn_tc"  PROCESS-WIDE: 1 = tcgen05 attention forward where seq % 128 == 0, 0 = mma.sync,
@@ -280,6 +291,15 @@ tgp_status tgp_bench_dominant_gemm(tgp_ctx* ctx, int32_t part, int32_t B, int32_
 tgp_status tgp_copy_stats(tgp_ctx* ctx, int64_t* bytes, int64_t* messages);
 
 tgp_status tgp_memory(tgp_ctx* ctx, int32_t part, int64_t* used, int64_t* reserved, int64_t* params);
+
+/* What the checkpoint mode changes in that plan (R1).  *stash =
+ * bytes of the bf16 dW-operand and skip stash: rows of the WHOLE mini-batch, kept from F until W_j,
+ * allocated in every checkpoint mode (deferred dW) -- checkpointing does NOT shrink it.
+ * *slots = bytes of the per-activation-slot fp32 buffers (layer outputs, pre-activations, LayerNorm
+ * statistics); *n_slots = slot count: 1 shared scratch + one per non-checkpointed micro-batch, i.e.
+ * m + 1 (never), 2 (except_last), 1 (always).  Only the slots are what checkpointing saves here.  Both
+ * byte counts are included in tgp_memory's *used.  Any pointer may be NULL. */
+tgp_status tgp_memory_breakdown(tgp_ctx* ctx, int32_t part, int64_t* stash, int64_t* slots, int32_t* n_slots);
 
 /* Profile-based balancing input: per-layer device time in ms of a
  * forward + backward of one micro-batch (B / chunks rows) of local partition `part`, median of

@@ -22,7 +22,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-I", CSRC, "-I", INC, "-Xptxas", "-v"] if os.environ.get("TGP_PTXAS_V") else \
         ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-I", CSRC, "-I", INC]
 
-SOURCES = ["plan.cpp", "runtime.cu", "kernels_ew.cu", "kernels_ln.cu", "gemm_simt.cu", "gemm_tc.cu", "task_stream.cu", "gemm_dw.cu", "kernels_attn.cu", "gemm_wide.cu"]
+SOURCES = ["plan.cpp", "runtime.cu", "kernels_ew.cu", "kernels_ln.cu", "gemm_simt.cu", "gemm_tc.cu", "task_stream.cu", "gemm_dw.cu", "gemm_dw_sgd.cu", "kernels_attn.cu", "gemm_wide.cu"]
 
 
 def _deps_hash(src):

@@ -1,6 +1,8 @@
 // Internal launcher declarations for the tgp CUDA kernels (host-callable; no torch types).
 // All launchers return 0 on success, a negative tgp_status on failure (message in tgp_last_error).
 #pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -24,6 +26,24 @@ struct TcMat {
 // operands stored [K][M] / [K][N], fp32 D; M, N multiples of 128.
 int gemm_dw(cudaStream_t st, const void* A, int64_t lda, const void* B, int64_t ldb, float* D, int64_t ldd, int M,
             int N, int K, bool accumulate);
+// Deferred dW GEMMs fused with plain SGD (gemm_dw_sgd.cu): for each GEMM,
+//   W[m][n] -= lr * sum_k A[k][m] B[k][n];  shadow[m][n] = bf16(W[m][n])
+// A [K][M], B [K][N] bf16 (MN-major operands, TMA zero-fills rows past K), W fp32 / shadow bf16
+// [M][N] with leading dimension ldw; M, N multiples of 128.  All GEMMs of the array run in one
+// persistent launch, tiles numbered GEMM after GEMM (tile0 = running sum of the tile counts, set by
+// the caller).  The gradient is not stored.
+struct alignas(64) WsGemm {
+  CUtensorMap a, b, w, sh;
+  int M, N, K, tiles_n, tiles, tile0;
+};
+bool wgrad_sgd_desc(WsGemm* d, const void* A, int64_t lda, const void* B, int64_t ldb, float* W, __nv_bfloat16* shadow,
+                    int64_t ldw, int M, int N, int K);
+// dev_descs: device copy of host_descs[ngemm]; lr: device scalar.
+int wgrad_sgd(cudaStream_t st, const WsGemm* dev_descs, const WsGemm* host_descs, int ngemm, const float* lr);
+// Plain SGD over parameter segments {offset, length} (device array seg[2 * nseg], elements) of the
+// arena: w -= lr g (fma, as sgd_kernel), shadow = bf16(w) when shadow != nullptr; lr: device scalar.
+int sgd_segments(cudaStream_t st, float* master, const float* grad, __nv_bfloat16* shadow, const int64_t* seg, int nseg,
+                 int64_t max_len, const float* lr);
 // Persistent tcgen05 GEMM for wide per-micro-batch GEMMs (gemm_wide.cu): same D = A B^T semantics and
 // epilogues as gemm_tc (B K-major, no second K-segment, no dW mode), one CTA per SM over 128 x 128 tiles.
 int gemm_wide(cudaStream_t st, const TcMat& A, bool a_mn, const TcMat& B, const GemmParams& p);

@@ -2,6 +2,8 @@
 // All reductions use fixed trees / fixed orders (deterministic: F' == F bitwise, reading Z21).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "host.h"
 #include "kernels.h"
@@ -288,10 +290,10 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, _
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 a = reinterpret_cast<float4*>(w)[i];
     const float4 b = reinterpret_cast<const float4*>(g)[i];
-    a.x -= lr * b.x;
-    a.y -= lr * b.y;
-    a.z -= lr * b.z;
-    a.w -= lr * b.w;
+    a.x = __fmaf_rn(-lr, b.x, a.x);  // the same fma as the fused W_j + SGD epilogue (gemm_dw_sgd.cu)
+    a.y = __fmaf_rn(-lr, b.y, a.y);
+    a.z = __fmaf_rn(-lr, b.z, a.z);
+    a.w = __fmaf_rn(-lr, b.w, a.w);
     reinterpret_cast<float4*>(w)[i] = a;
     if (sh) {
       __nv_bfloat162* s2 = reinterpret_cast<__nv_bfloat162*>(sh) + 2 * i;
@@ -308,6 +310,27 @@ int sgd_step(cudaStream_t st, float* master, const float* grad, __nv_bfloat16* s
   const int64_t n4 = n / 4;
   const int blocks = (int)(n4 / 256 + 1 < 148 * 8 ? n4 / 256 + 1 : 148 * 8);
   return launch("sgd", sgd_kernel, dim3(blocks), dim3(256), st, false, master, grad, shadow, n4, lr);
+}
+
+__global__ void sgd_segments_kernel(float* __restrict__ w, const float* __restrict__ g, __nv_bfloat16* __restrict__ sh,
+                                    const int64_t* __restrict__ seg, const float* __restrict__ lrp) {
+  const int64_t off = seg[2 * blockIdx.y], len = seg[2 * blockIdx.y + 1];
+  const float lr = *lrp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    const float a = __fmaf_rn(-lr, g[off + i], w[off + i]);
+    w[off + i] = a;
+    if (sh) sh[off + i] = __float2bfloat16_rn(a);
+  }
+}
+int sgd_segments(cudaStream_t st, float* master, const float* grad, __nv_bfloat16* shadow, const int64_t* seg, int nseg,
+                 int64_t max_len, const float* lr) {
+  if (nseg <= 0) return 0;
+  if (nseg > 65535) {
+    set_error("sgd_segments: %d segments (max 65535)", nseg);
+    return -5;
+  }
+  const int bx = (int)std::min<int64_t>((max_len + 255) / 256, 64);
+  return launch("sgd_segments", sgd_segments_kernel, dim3(bx, nseg), dim3(256), st, false, master, grad, shadow, seg, lr);
 }
 
 __global__ void cast_bf16_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ d, int64_t n) {

@@ -291,6 +291,7 @@ int ln_fwd_cl(cudaStream_t st, bool pdl, const float* x, int64_t ldx, int rows, 
                           ldh, (int)h_bf16, mean, rstd);
   L_(32) L_(64) L_(128)
 #undef L_
+  set_error("ln_fwd_cl: no cluster shape for d=%d", d);
   return -5;
 }
 
@@ -298,13 +299,17 @@ int ln_bwd_cl(cudaStream_t st, bool pdl, const float* dh, const float* x, const 
               const float* gamma, const float* dy, float* dx, int rows, int d, int rowblocks, float* dgp, float* dbp,
               void* op, bool op_bf16, float* opsum) {
   int NQ, CL;
-  if (ln_cluster_shape(d, &NQ, &CL)) return -5;
+  if (ln_cluster_shape(d, &NQ, &CL)) {
+    set_error("ln_bwd_cl: no cluster shape for d=%d", d);
+    return -5;
+  }
 #define L_(N)                                                                                                   \
   if (NQ == N)                                                                                                  \
     return launch_cluster("ln_bwd_cl", ln_bwd_cl_kernel<N>, CL, rowblocks, st, pdl, dh, x, mean, rstd, gamma, dy, \
                           dx, rows, d, dgp, dbp, op, (int)op_bf16, opsum);
   L_(32) L_(64) L_(128)
 #undef L_
+  set_error("ln_bwd_cl: no cluster shape for d=%d", d);
   return -5;
 }
 
@@ -386,7 +391,10 @@ __global__ void __launch_bounds__(128) colwise_kernel(const float* __restrict__ 
 int colwise(cudaStream_t st, bool pdl, const float* src, int64_t lds, const float* z, int rows, int d, int act,
             uint32_t drop_thresh, float drop_scale, uint64_t seed, const uint32_t* step, uint32_t site,
             int64_t row_global0, void* out, int64_t ldo, bool out_bf16, float* colsum) {
-  if (d % 4 || lds % 4 || ldo % 4) return -5;
+  if (d % 4 || lds % 4 || ldo % 4) {
+    set_error("colwise: d=%d, lds=%lld, ldo=%lld must be multiples of 4", d, (long long)lds, (long long)ldo);
+    return -5;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((d / 4 + 31) / 32, (rows + 15) / 16, 1);
   cfg.blockDim = dim3(128, 1, 1);

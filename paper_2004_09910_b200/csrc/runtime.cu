@@ -336,6 +336,7 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
   t.seed = c->seed;
   t.step = s.dstep;
   t.sleep_ns = c->st_sleep_ns;
+  t.inflight = c->st_inflight;
   if (getenv("TGP_ST_DEBUG")) {  // diagnostics: per-CTA, per-phase %globaltimer stamps
     const size_t nd = (size_t)s.st_clusters * 4 * 2 * t.L * ST_DBG_SLOTS;
     if (!s.st_dbg) {
@@ -752,10 +753,40 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
 
 // W_j: deferred weight gradients g^j = sum_i g_i^j as one GEMM per weight over the stacked
 // micro-batches, plus fixed-order reductions of the per-micro-batch column partials.
-static int exec_wgrad(tgp_ctx* c, Stage& s, int B) {
+// Descriptors of the fused W_j + SGD GEMMs for batch B (the operand maps have K = B rows: TMA
+// zero-fills past them), uploaded on the compute stream (stream-ordered before the W task).
+static int ensure_ws(tgp_ctx* c, Stage& s, int B) {
+  if (s.ws_B == B || s.ws_layers.empty()) return 0;
+  s.ws_host.assign(2 * s.ws_layers.size(), WsGemm{});
+  int tile0 = 0;
+  for (size_t q = 0; q < s.ws_layers.size(); ++q) {
+    const LayerRT& L = c->layers[s.ws_layers[q]];
+    const int d = L.L.d_in, H = L.L.d_hidden;
+    WsGemm& g1 = s.ws_host[2 * q];
+    WsGemm& g2 = s.ws_host[2 * q + 1];
+    // dW1[h][k] = sum_r dA[r][h] LN(x)[r][k];  dW2[f][h] = sum_r dY[r][f] G[r][h]
+    if (!wgrad_sgd_desc(&g1, L.dAop, H, L.Hop, d, mparam(s, L, 2), s.shadow + L.poff[2], d, H, d, B) ||
+        !wgrad_sgd_desc(&g2, L.dYop, d, L.Gop, H, mparam(s, L, 4), s.shadow + L.poff[4], H, d, H, B))
+      return TGP_E_CUDA;
+    g1.tile0 = tile0;
+    tile0 += g1.tiles;
+    g2.tile0 = tile0;
+    tile0 += g2.tiles;
+  }
+  TGP_CUDA_TRY(cudaMemcpyAsync(s.ws_dev, s.ws_host.data(), s.ws_host.size() * sizeof(WsGemm), cudaMemcpyHostToDevice,
+                               s.comp));
+  s.ws_B = B;
+  return 0;
+}
+
+// W_j.  fused: SGD applied here (tgp_backward_step): the fused weight matrices' dW accumulators update
+// the master / shadow directly (wgrad_sgd), the other parameters' gradients are stored as usual and
+// then stepped by sgd_segments; requires fresh gradients.
+static int exec_wgrad(tgp_ctx* c, Stage& s, int B, bool fused = false) {
   const bool acc = !s.grads_fresh;
   for (int l = s.l0; l < s.l1; ++l) {
     LayerRT& L = c->layers[l];
+    if (fused && std::find(s.ws_layers.begin(), s.ws_layers.end(), l) != s.ws_layers.end()) continue;
     const int din = L.L.d_in, dout = L.L.d_out;
     EpiParams e{};
     e.mode = EPI_DW;
@@ -823,6 +854,14 @@ static int exec_wgrad(tgp_ctx* c, Stage& s, int B) {
   // every bias / LayerNorm / BatchNorm column-partial reduction of the partition in one launch
   if (s.n_red > 0) {
     TGP_TRY(reduce_partials_multi(s.comp, (const RedItem*)s.red_items, s.n_red, s.red_maxd, c->m * c->pb, acc));
+    c->kernels++;
+  }
+  if (fused) {
+    if (!s.ws_layers.empty()) {
+      TGP_TRY(wgrad_sgd(s.comp, s.ws_dev, s.ws_host.data(), (int)s.ws_host.size(), s.dlr));
+      c->kernels++;
+    }
+    TGP_TRY(sgd_segments(s.comp, s.master, s.grad, s.shadow, s.seg_dev, s.n_seg, s.seg_maxlen, s.dlr));
     c->kernels++;
   }
   s.grads_fresh = false;
@@ -1090,12 +1129,23 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       Stage& s = *sp;
       cudaEvent_t ta = nullptr;
       trace_begin(c, s, s.comp, 0, rc.kind, 0, &ta);
-      // the W graph bakes in the accumulate flag -> only replay when grads are fresh
-      if (s.grads_fresh) {
+      if (c->fuse_sgd && s.grads_fresh && c->bf16) {
+        // W_j + SGD (tgp_backward_step): the learning rate is a device scalar, so the graph replays
+        TGP_TRY(ensure_ws(c, s, B));
+        TGP_CUDA_TRY(cudaMemcpyAsync(s.dlr, &c->lr_host, 4, cudaMemcpyHostToDevice, s.comp));
+        TGP_TRY(run_task(c, s, s.gWs, B, [&] { return exec_wgrad(c, s, B, true); }));
+        s.grads_fresh = true;  // consumed by the fused step
+      } else if (s.grads_fresh) {
+        // the W graph bakes in the accumulate flag -> only replay when grads are fresh
         TGP_TRY(run_task(c, s, s.gW, B, [&] { return exec_wgrad(c, s, B); }));
         s.grads_fresh = false;
       } else {
         TGP_TRY(exec_wgrad(c, s, B));
+      }
+      if (c->fuse_sgd && !s.grads_fresh) {  // tgp_backward_step without the fused path: W_j, then SGD
+        TGP_TRY(sgd_step(s.comp, s.master, s.grad, s.shadow, s.n_elems, c->lr_host));
+        c->kernels++;
+        s.grads_fresh = true;
       }
       trace_end(c, s, s.comp, 0, rc.kind, 0, ta);
       c->issue_log.push_back(rc);

@@ -82,6 +82,8 @@ struct Stage {
   Pool pool;
   void* arena = nullptr;
   size_t extra_bytes = 0;  // device allocations outside the pool (arena, descriptors, tables)
+  size_t stash_bytes = 0;  // of pool.used: bf16 dW operand + skip stash (whole mini-batch, every mode)
+  size_t slot_bytes = 0;   // of pool.used: per-activation-slot fp32 buffers (count set by the checkpoint mode)
   ArenaView self;
   float* out = nullptr;     // [max_batch][d_out] stage output (message source)
   float* dx_out = nullptr;  // [max_batch][d_in] input gradient (message source)
@@ -130,6 +132,17 @@ struct Stage {
   std::vector<TaskGraph> gF, gB;
   TaskGraph gW;
   bool grads_fresh = true;
+  // W_j fused with SGD (tgp_backward_step; gemm_dw_sgd.cu): the bf16 RESMLP weight matrices go through
+  // wgrad_sgd, every other parameter through sgd_segments
+  std::vector<int> ws_layers;       // RESMLP layers whose W1 / W2 are fused
+  std::vector<WsGemm> ws_host;      // descriptors for batch ws_B (operand maps have K = B rows)
+  WsGemm* ws_dev = nullptr;         // device copy
+  int ws_B = -1;
+  int64_t* seg_dev = nullptr;       // non-fused parameter segments {offset, length}
+  int n_seg = 0;
+  int64_t seg_maxlen = 0;
+  float* dlr = nullptr;             // device learning rate of the fused step
+  TaskGraph gWs;
 };
 
 struct TraceRec {
@@ -151,6 +164,8 @@ struct tgp_ctx {
   uint32_t step = 0;
   uint32_t seq = 0;
   int state = 0;  // 0 created, 1 forwarded, 2 backwarded
+  bool fuse_sgd = false;  // inside tgp_backward_step: W_j applies SGD with lr_host (no gradient stored)
+  float lr_host = 0.0f;
   int cur_B = 0;
   std::vector<tgp::Stage*> local;       // by partition (nullptr if remote)
   std::vector<tgp::ArenaView> view;     // by partition
@@ -166,6 +181,7 @@ struct tgp_ctx {
   bool stream = true;
   bool gemm_wide = true;      // per-micro-batch GEMMs with >= 256 rows through the persistent gemm_wide kernel (option "gemm_wide")
   bool dw_persistent = true;  // deferred dW through the persistent gemm_dw kernel (option "dw_persistent")
+  unsigned st_inflight = 0;  // stream kernel: max weight tiles in flight per CTA (0 = ring-limited; "stream_inflight")
   unsigned st_sleep_ns = 32;  // stream kernel: back-off between dependency polls (option "stream_poll_ns")
   // Table 1 ablation toggles: 0 / false = the torchgpipe design
   uint64_t order_seed = 0;   // "ablate_order": backward tasks in a seeded random topological order

@@ -233,6 +233,13 @@ __global__ void __launch_bounds__(ST_THREADS, 1) task_stream_kernel(const __grid
         while (wp < NP) {  // weights: run ahead as far as the rings allow
           const int s = t.bwd ? it % NST_BWD : it % NST_FWD, r = t.bwd ? it / NST_BWD : it / NST_FWD;
           if (!mbar_test_wait(smem_u32(&empty[s]), (uint32_t)((r & 1) ^ 1))) break;
+          if (t.inflight && (int)t.inflight < NST && it >= (int)t.inflight) {
+            // at most `inflight` weight tiles in flight: tile it - inflight has landed (its stage is
+            // not re-armed before tile it - inflight + NST > it is issued, so the parity is unambiguous)
+            const int o = it - (int)t.inflight;
+            const int so = t.bwd ? o % NST_BWD : o % NST_FWD, ro = t.bwd ? o / NST_BWD : o / NST_FWD;
+            if (!mbar_test_wait(smem_u32(&full[so]), (uint32_t)(ro & 1))) break;
+          }
           const Ph P = phase_of(t, wp);
           const int nkb = P.K / (SK * 64);
           const int kc = (rank * nkb + wkb) * 64;

@@ -64,6 +64,7 @@ struct STask {
   // [grid][2L][ST_DBG_SLOTS] (TGP_ST_DEBUG); they do not change any result
   unsigned long long* dbg;
   unsigned sleep_ns;  // back-off between dependency polls
+  unsigned inflight;  // max weight tiles issued but not landed per CTA (0 = limited by the ring only)
 };
 constexpr int ST_DBG_SLOTS = 12;
 

@@ -60,6 +60,7 @@ _SIGS = {
     "tgp_ce_loss_grad": [_P, _P, _P, _I32, _P, ctypes.POINTER(ctypes.c_double)],
     "tgp_backward": [_P, _P, _P],
     "tgp_step": [_P, ctypes.c_float],
+    "tgp_backward_step": [_P, _P, _P, ctypes.c_float],
     "tgp_num_params": [_P, ctypes.POINTER(_I32)],
     "tgp_param_info": [_P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I64)],
     "tgp_set_param": [_P, _I32, _P],
@@ -79,6 +80,7 @@ _SIGS = {
     "tgp_stream_enabled": [_P, _I32, ctypes.POINTER(_I32)],
     "tgp_profile_layers": [_P, _I32, _I32, _I32, ctypes.POINTER(ctypes.c_double)],
     "tgp_memory": [_P, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
+    "tgp_memory_breakdown": [_P, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I32)],
     "tgp_test_gemm_bf16": [_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P],
     "tgp_bench_transport": [_I32, _I32, _I64, _I32, _I32, ctypes.POINTER(ctypes.c_double),
                             ctypes.POINTER(ctypes.c_double)],
@@ -247,6 +249,11 @@ class Pipeline:
     def step(self, lr):
         _check(lib().tgp_step(self.h, ctypes.c_float(lr)), "tgp_step")
 
+    def backward_step(self, dy, lr, dx=None):
+        """tgp_backward + tgp_step(lr) with SGD fused into W_j (fused weight gradients not stored)."""
+        _ready(dy, dx)
+        _check(lib().tgp_backward_step(self.h, _ptr(dy), _ptr(dx), ctypes.c_float(lr)), "tgp_backward_step")
+
     # ---- parameters
     def param_info(self, idx):
         layer, part, numel = _I32(), _I32(), _I64()
@@ -321,6 +328,14 @@ class Pipeline:
         u, r, p = _I64(), _I64(), _I64()
         _check(lib().tgp_memory(self.h, part, ctypes.byref(u), ctypes.byref(r), ctypes.byref(p)), "tgp_memory")
         return {"used": u.value, "reserved": r.value, "params": p.value}
+
+    def memory_breakdown(self, part):
+        """What checkpointing changes (tgp_memory_breakdown): dict(stash, slots, n_slots) -- the bf16
+        dW-operand / skip stash (whole mini-batch, every mode) and the per-slot fp32 activations."""
+        st, sl, ns = _I64(), _I64(), _I32()
+        _check(lib().tgp_memory_breakdown(self.h, part, ctypes.byref(st), ctypes.byref(sl), ctypes.byref(ns)),
+               "tgp_memory_breakdown")
+        return {"stash": st.value, "slots": sl.value, "n_slots": ns.value}
 
     def copy_stats(self):
         """(payload bytes, messages) pushed by this process since creation (tgp_copy_stats)."""

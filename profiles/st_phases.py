@@ -21,6 +21,7 @@ bwd = int(opts.get("bwd", 0))
 layers = C.resmlp_stack(blocks, 4096)
 P = Pipeline(layers, chunks=32, devices=[0], balance=[blocks], checkpoint="never", max_batch=512, dtype="bf16", seed=1)
 P.set_option("stream_poll_ns", int(opts.get("poll", 32)))
+P.set_option("stream_inflight", int(opts.get("inflight", 0)))
 P.set_option("graphs", 0)
 P.init_params(1)
 X = torch.randn(512, 4096, device="cuda")

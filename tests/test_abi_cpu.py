@@ -85,6 +85,12 @@ def test_create_validates_before_touching_cuda(L):
     layers[0]["stash"], layers[2]["pop"] = -1, 0
     with pytest.raises(L.TgpError):
         L.Pipeline(layers, chunks=2, devices=[0], balance=[len(layers)], max_batch=4, dtype="bf16")
+    # fp32 widths must be multiples of 4 (float4 row kernels): rejected at create, with a message
+    for d_in, d_out in ((3, 4), (4, 6)):
+        layers = [C.layer("linear", d_in, d_out)]
+        with pytest.raises(L.TgpError) as ei:
+            L.Pipeline(layers, chunks=1, devices=[0], balance=[1], max_batch=4, dtype="fp32")
+        assert "(-5)" in str(ei.value) and "multiples of 4" in str(ei.value)
 
 
 def test_create_validates_gpt2_layers(L):

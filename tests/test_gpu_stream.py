@@ -246,3 +246,18 @@ def test_memory_plan_checkpointing_saves_activations():
     assert slot > 0
     # a slot holds the block outputs, pre-activations and LN statistics of a 16-row micro-batch
     assert abs((use["except_last"]["used"] - use["always"]["used"]) - slot) <= 0.05 * slot
+    # what the checkpoint mode changes is exactly the slot bytes; the bf16 dW-operand stash (R1)
+    # is the same in every mode (tgp_memory_breakdown)
+    br = {}
+    for mode in ("always", "except_last", "never"):
+        P = Pipeline(layers, chunks=8, devices=[0], checkpoint=mode, max_batch=128, dtype="bf16")
+        br[mode] = P.memory_breakdown(0)
+        P.close()
+    assert [br[m]["n_slots"] for m in ("always", "except_last", "never")] == [1, 2, 9]
+    assert br["always"]["stash"] == br["never"]["stash"] > 0
+    # 4 RESMLP blocks x 4 bf16 operands (Hop, Gop, dAop, dYop) x 128 rows x 1024
+    assert br["always"]["stash"] == 4 * 4 * 128 * 1024 * 2
+    per_slot = br["always"]["slots"]
+    assert br["never"]["slots"] == 9 * per_slot and br["except_last"]["slots"] == 2 * per_slot
+    dslots = br["never"]["slots"] - br["always"]["slots"]
+    assert abs((use["never"]["used"] - use["always"]["used"]) - dslots) <= 0.01 * dslots
