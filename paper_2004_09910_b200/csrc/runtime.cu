@@ -295,6 +295,7 @@ static int st_build_desc(tgp_ctx* c, Stage& s, int B) {
       P.pbt = Ly.pbt + po * d;
     }
   }
+  if (s.comp2) TGP_CUDA_TRY(cudaStreamSynchronize(s.comp2));  // a lane-1 task may read the old descriptors
   TGP_CUDA_TRY(cudaMemcpyAsync(s.st_layers, hl.data(), hl.size() * sizeof(SLayer), cudaMemcpyHostToDevice, s.comp));
   TGP_CUDA_TRY(cudaMemcpyAsync(s.st_micro, hm.data(), hm.size() * sizeof(SMicro), cudaMemcpyHostToDevice, s.comp));
   TGP_CUDA_TRY(cudaStreamSynchronize(s.comp));
@@ -316,7 +317,9 @@ static int st_refold(tgp_ctx* c, Stage& s, int B) {
   return 0;
 }
 
-static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd) {
+// lane: 0 = full grid on comp; 1 = half grid on comp (a paired B); 2 = half grid on comp2 with the
+// lane-1 counters / statistics (a paired F', beside the lane-1 B)
+static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd, int lane = 0) {
   const LayerRT& L0 = c->layers[s.l0];
   STask t{};
   t.L = s.l1 - s.l0;
@@ -327,17 +330,18 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
   t.M = M;
   t.r0 = r0;
   t.bwd = bwd ? 1 : 0;
+  t.nv = lane ? 2 : 1;
   t.gy_top = s.self.grad_in + (size_t)r0 * s.d_out;
   t.dx_bottom = s.dx_out + (size_t)r0 * s.d_in;
   t.gbuf0 = s.gbuf[0];
   t.gbuf1 = s.gbuf[1];
-  t.stats = s.st_stats;
-  t.cnt = s.st_cnt;
+  t.stats = lane == 2 ? s.st_stats2 : s.st_stats;
+  t.cnt = lane == 2 ? s.st_cnt2 : s.st_cnt;
   t.seed = c->seed;
   t.step = s.dstep;
   t.sleep_ns = c->st_sleep_ns;
   t.inflight = c->st_inflight;
-  if (getenv("TGP_ST_DEBUG")) {  // diagnostics: per-CTA, per-phase %globaltimer stamps
+  if (lane == 0 && getenv("TGP_ST_DEBUG")) {  // diagnostics: per-CTA, per-phase %globaltimer stamps
     const size_t nd = (size_t)s.st_clusters * 4 * 2 * t.L * ST_DBG_SLOTS;
     if (!s.st_dbg) {
       TGP_CUDA_TRY(cudaMalloc(&s.st_dbg, nd * 8));
@@ -346,7 +350,7 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
     t.dbg = s.st_dbg;
   }
   c->kernels += 1;  // the task kernel (it resets its dependency counters itself)
-  return task_stream_launch(s.comp, t, s.st_clusters);
+  return task_stream_launch(lane == 2 ? s.comp2 : s.comp, t, lane ? s.st_half : s.st_clusters);
 }
 
 // F_{i,j} (and F'_{i,j}: identical kernels and launch configuration -> bitwise identical output)
@@ -872,10 +876,11 @@ static int exec_wgrad(tgp_ctx* c, Stage& s, int B, bool fused = false) {
 // Each task's kernel sequence is captured once into a CUDA graph (per micro-batch, per batch size)
 // and replayed: one host launch per task instead of ~3 per layer.
 template <typename Fn>
-static int run_task(tgp_ctx* c, Stage& s, TaskGraph& tg, int B, Fn&& fn) {
+static int run_task(tgp_ctx* c, Stage& s, TaskGraph& tg, int B, Fn&& fn, cudaStream_t st = nullptr) {
+  if (!st) st = s.comp;
   if (!c->use_graphs) return fn();
   if (tg.exec && tg.B == B) {
-    TGP_CUDA_TRY(cudaGraphLaunch(tg.exec, s.comp));
+    TGP_CUDA_TRY(cudaGraphLaunch(tg.exec, st));
     c->kernels += tg.kernels;
     return 0;
   }
@@ -884,10 +889,10 @@ static int run_task(tgp_ctx* c, Stage& s, TaskGraph& tg, int B, Fn&& fn) {
     tg.exec = nullptr;
   }
   const int64_t k0 = c->kernels;
-  TGP_CUDA_TRY(cudaStreamBeginCapture(s.comp, cudaStreamCaptureModeThreadLocal));
+  TGP_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   int rc = fn();
   cudaGraph_t graph = nullptr;
-  cudaError_t ce = cudaStreamEndCapture(s.comp, &graph);
+  cudaError_t ce = cudaStreamEndCapture(st, &graph);
   if (rc) {
     if (graph) cudaGraphDestroy(graph);
     return rc;
@@ -899,7 +904,7 @@ static int run_task(tgp_ctx* c, Stage& s, TaskGraph& tg, int B, Fn&& fn) {
   tg.B = B;
   tg.kernels = c->kernels - k0;
   c->kernels = k0;
-  TGP_CUDA_TRY(cudaGraphLaunch(tg.exec, s.comp));
+  TGP_CUDA_TRY(cudaGraphLaunch(tg.exec, st));
   c->kernels += tg.kernels;
   return 0;
 }
@@ -1096,6 +1101,34 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       Stage* sp = c->local[j];
       if (!sp) return 0;
       Stage& s = *sp;
+      const bool stream_task = use_stream(c, s, M);
+      if (stream_task && s.st_micro_B != B) TGP_TRY(st_build_desc(c, s, B));
+      if (rc.kind == K_RECOMPUTE && s.pair_ok && s.hoisted[i] == 1) {
+        // F'_{i,j} was issued on lane 1 beside B_{i+1,j} (see K_B): only the record remains
+        c->issue_log.push_back(rc);
+        return 0;
+      }
+      // F' / B pairing: F'_{i-1,j} depends only on the stage input and the weights, not on B_{i,j},
+      // so it is hoisted onto lane 1 and runs beside B_{i,j}, both on half grids; issued before B's
+      // gradient wait so it does not wait for the downstream partition
+      bool paired = false;
+      if (rc.kind == K_B && stream_task && s.pair_ok && c->pair && c->order_seed == 0 && i >= 2 &&
+          checkpointed(i - 1, c->m, c->ckpt) && !s.hoisted[i - 1]) {
+        int pr0 = 0, pM = 0;
+        micro_rows(c, B, i - 1, &pr0, &pM);
+        if (use_stream(c, s, pM)) {
+          TGP_CUDA_TRY(cudaEventRecord(s.ev_pair, s.comp));  // after B_{i+1,j}, the last reader of the slot
+          TGP_CUDA_TRY(cudaStreamWaitEvent(s.comp2, s.ev_pair, 0));
+          cudaEvent_t tr = nullptr;
+          trace_begin(c, s, s.comp2, 3, K_RECOMPUTE, i - 1, &tr);
+          TGP_TRY(run_task(c, s, s.gR2[i - 2], B, [&] { return exec_task_stream(c, s, i - 1, pr0, pM, false, 2); },
+                           s.comp2));
+          trace_end(c, s, s.comp2, 3, K_RECOMPUTE, i - 1, tr);  // before rdone: B_{i-1} starts after it
+          TGP_CUDA_TRY(cudaEventRecord(s.rdone[i - 2], s.comp2));
+          s.hoisted[i - 1] = 1;
+          paired = true;
+        }
+      }
       if (rc.kind == K_F && j > 0 && c->skip_wait_part != j) TGP_TRY(wait_flag(c, s.comp, flag_fwd(s.self, i), seq));
       // relay (ablation): a partition between stash and pop takes the skip tensor as a tuple input
       // of F and its gradient as a tuple input of B
@@ -1108,10 +1141,14 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
         for (const Route& R : c->routes)
           if ((R.src == j && R.dst != j) || relays(R)) TGP_TRY(wait_flag(c, s.comp, flag_dskip(c, s.self, R.id, i), seq));
       }
+      if (rc.kind == K_B && s.pair_ok && s.hoisted[i] == 1) TGP_CUDA_TRY(cudaStreamWaitEvent(s.comp, s.rdone[i - 1], 0));
+      if (rc.kind == K_RECOMPUTE && s.pair_ok) s.hoisted[i] = 2;  // issued in place
       cudaEvent_t ta = nullptr;
       trace_begin(c, s, s.comp, 0, rc.kind, i, &ta);
-      if (use_stream(c, s, M) && s.st_micro_B != B) TGP_TRY(st_build_desc(c, s, B));
-      if (rc.kind == K_B) {
+      if (rc.kind == K_B && paired) {
+        TGP_TRY(run_task(c, s, s.gB2[i - 1], B, [&] { return exec_task_stream(c, s, i, r0, M, true, 1); }));
+        TGP_CUDA_TRY(cudaEventRecord(s.bdone[i - 1], s.comp));
+      } else if (rc.kind == K_B) {
         TGP_TRY(run_task(c, s, s.gB[i - 1], B, [&] { return exec_backward(c, s, i, r0, M); }));
         TGP_CUDA_TRY(cudaEventRecord(s.bdone[i - 1], s.comp));
       } else {
@@ -1168,7 +1205,7 @@ static bool streams_idle(tgp_ctx* c) {
   for (Stage* q : c->local) {
     if (!q) continue;
     cudaSetDevice(q->dev);
-    for (cudaStream_t st : {q->comp, q->cact, q->cskip})
+    for (cudaStream_t st : {q->comp, q->cact, q->cskip, q->comp2 ? q->comp2 : q->comp})
       if (cudaStreamQuery(st) == cudaErrorNotReady) return false;
   }
   return true;
@@ -1183,7 +1220,7 @@ static int sync_with_watchdog(tgp_ctx* c) {
     Stage* sp = c->local[j];
     if (!sp) continue;
     TGP_CUDA_TRY(cudaSetDevice(sp->dev));
-    for (cudaStream_t st : {sp->comp, sp->cact, sp->cskip}) {
+    for (cudaStream_t st : {sp->comp, sp->cact, sp->cskip, sp->comp2 ? sp->comp2 : sp->comp}) {
       while (true) {
         const cudaError_t e = cudaStreamQuery(st);
         if (e == cudaSuccess) break;

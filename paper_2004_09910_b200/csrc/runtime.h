@@ -125,6 +125,18 @@ struct Stage {
   void* st_uc = nullptr;      // [32][d] bf16: backward dG operand [u | n]
   float* st_c2part = nullptr; // [L][d/256][H] partial column sums of W2
   bool fold_dirty = true;     // weights / LN parameters changed since st_fold was computed
+  // F' / B pairing (option "pair_recompute"): F'_{i-1,j} runs on lane 1 (comp2) beside B_{i,j} on
+  // lane 0, both on a half grid (st_half clusters, two output slabs each); lane 1 has its own
+  // counters / statistics scratch.  Checkpointed micro-batches alternate two scratch slots.
+  bool pair_ok = false;
+  int st_half = 0;
+  cudaStream_t comp2 = nullptr;
+  unsigned* st_cnt2 = nullptr;
+  float* st_stats2 = nullptr;
+  cudaEvent_t ev_pair = nullptr;      // recorded on comp before a paired B: lane 1 waits for it
+  std::vector<cudaEvent_t> rdone;     // per micro-batch: its hoisted F' finished (recorded on comp2)
+  std::vector<char> hoisted;          // per micro-batch: F' already issued on lane 1 in this call
+  std::vector<TaskGraph> gR2, gB2;    // paired-task graphs (half grid)
   unsigned long long* st_dbg = nullptr;  // diagnostics (TGP_ST_DEBUG): [grid][2L][ST_DBG_SLOTS]
   cudaEvent_t* prof_ev = nullptr;  // tgp_profile_layers: per-layer boundary events (forward, then backward)
   void* red_items = nullptr;  // device RedItem[n_red]: column-partial -> gradient reductions of W_j
@@ -179,6 +191,8 @@ struct tgp_ctx {
   bool use_graphs = true, use_pdl = true, trace = false, poison = false, prefetch = false;
   bool l2pf = false;
   bool stream = true;
+  bool pair = true;           // F'_{i-1,j} beside B_{i,j} on half grids (option "pair_recompute")
+  bool pair_slots = false;    // checkpointed micro-batches alternate two scratch slots (set at create)
   bool gemm_wide = true;      // per-micro-batch GEMMs with >= 256 rows through the persistent gemm_wide kernel (option "gemm_wide")
   bool dw_persistent = true;  // deferred dW through the persistent gemm_dw kernel (option "dw_persistent")
   unsigned st_inflight = 0;  // stream kernel: max weight tiles in flight per CTA (0 = ring-limited; "stream_inflight")

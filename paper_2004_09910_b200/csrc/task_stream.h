@@ -51,6 +51,7 @@ struct STask {
   const SLayer* layers;  // [L]
   const SMicro* micro;   // [L], this micro-batch
   int L, d, H, M, r0, bwd;
+  int nv;                // output slabs per cluster: 1 = full grid, 2 = half grid (a paired task, runtime.cu)
   const float* gy_top;   // backward: incoming output gradient rows [M][d]
   float* dx_bottom;      // backward: input gradient rows [M][d] (message source)
   float* gbuf0;          // backward: inter-block gradient ping-pong [16][d]
@@ -70,7 +71,9 @@ constexpr int ST_DBG_SLOTS = 12;
 
 int task_stream_smem();
 int task_stream_counter_bytes(int L);
-// Clusters of 4 the device can co-schedule (0 if the kernel cannot run there).
+// Clusters of 4 the device can co-schedule (0 if the kernel cannot run there).  A task launched on
+// `clusters` clusters with t.nv = 2 covers 2 x clusters output slabs (half grid: two such tasks run
+// side by side).
 int task_stream_max_clusters(int dev);
 int task_stream_launch(cudaStream_t st, const STask& t, int clusters);
 // c[h] = sum_k gamma[k] W1[h][k], e[h] = sum_k beta[k] W1[h][k] + b1[h] (fixed-order fp32 sums over

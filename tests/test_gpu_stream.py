@@ -230,34 +230,33 @@ def test_profile_based_balance():
 
 
 def test_memory_plan_checkpointing_saves_activations():
-    # checkpointing keeps only the stage input per micro-batch (the receive slab) plus one
-    # scratch activation slot, instead of every micro-batch's intermediates; the static plan shows it
+    # checkpointing keeps only the stage input per micro-batch (the receive slab) plus the
+    # scratch activation slot(s), instead of every micro-batch's intermediates; the static plan shows
+    # it.  With F' / B pairing (the stream kernel) checkpointed micro-batches alternate TWO scratch
+    # slots (F'_{i-1} recomputes while B_i reads F'_i's).  What the checkpoint mode changes is exactly
+    # the slot bytes; the bf16 dW-operand stash (R1) is the same in every mode (tgp_memory_breakdown).
     from paper_2004_09910_b200 import Pipeline
 
     layers = C.resmlp_stack(4, 1024)
-    use = {}
+    use, br = {}, {}
     for mode in ("always", "except_last", "never"):
         P = Pipeline(layers, chunks=8, devices=[0], checkpoint=mode, max_batch=128, dtype="bf16")
         use[mode] = P.memory(0)
-        P.close()
-    assert use["always"]["params"] == use["never"]["params"]
-    # slots: always = the shared scratch slot; except_last = scratch + micro-batch m; never = scratch + m
-    slot = (use["never"]["used"] - use["always"]["used"]) / 8
-    assert slot > 0
-    # a slot holds the block outputs, pre-activations and LN statistics of a 16-row micro-batch
-    assert abs((use["except_last"]["used"] - use["always"]["used"]) - slot) <= 0.05 * slot
-    # what the checkpoint mode changes is exactly the slot bytes; the bf16 dW-operand stash (R1)
-    # is the same in every mode (tgp_memory_breakdown)
-    br = {}
-    for mode in ("always", "except_last", "never"):
-        P = Pipeline(layers, chunks=8, devices=[0], checkpoint=mode, max_batch=128, dtype="bf16")
         br[mode] = P.memory_breakdown(0)
         P.close()
-    assert [br[m]["n_slots"] for m in ("always", "except_last", "never")] == [1, 2, 9]
-    assert br["always"]["stash"] == br["never"]["stash"] > 0
+    assert use["always"]["params"] == use["never"]["params"]
+    # always: 2 scratch; except_last: 2 scratch + micro-batch m; never: 1 scratch + m
+    assert [br[m]["n_slots"] for m in ("always", "except_last", "never")] == [2, 3, 9]
+    assert br["always"]["stash"] == br["except_last"]["stash"] == br["never"]["stash"] > 0
     # 4 RESMLP blocks x 4 bf16 operands (Hop, Gop, dAop, dYop) x 128 rows x 1024
     assert br["always"]["stash"] == 4 * 4 * 128 * 1024 * 2
-    per_slot = br["always"]["slots"]
-    assert br["never"]["slots"] == 9 * per_slot and br["except_last"]["slots"] == 2 * per_slot
-    dslots = br["never"]["slots"] - br["always"]["slots"]
-    assert abs((use["never"]["used"] - use["always"]["used"]) - dslots) <= 0.01 * dslots
+    per_slot = br["always"]["slots"] / 2
+    assert per_slot > 0
+    for mode in ("except_last", "never"):
+        assert br[mode]["slots"] == br[mode]["n_slots"] * per_slot
+        dslots = br[mode]["slots"] - br["always"]["slots"]
+        assert abs((use[mode]["used"] - use["always"]["used"]) - dslots) <= 0.01 * dslots
+    # without the stream kernel (no pairing) the shared scratch slot is single again
+    P = Pipeline(C.resmlp_stack(4, 1024), chunks=4, devices=[0], checkpoint="always", max_batch=128, dtype="bf16")
+    assert P.memory_breakdown(0)["n_slots"] == 1  # 32-row micro-batches: no stream kernel, no pairing
+    P.close()
