@@ -255,6 +255,13 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *             2 = by message size: copy engine from 16 KiB up (the B200 crossover of
  *             tgp_bench_transport; default).  Skip tensors always use the push kernel (bf16
  *             conversion).  Same bytes either way: results are bitwise identical.
+ *  "fused_send" 1 (default) = with transport 2, a persistent stream-kernel task stores its boundary
+ *             tensor (F: the last block's output, B: the input gradient) straight into the
+ *             neighbour partition's receive slab and release-stores the flag itself at system
+ *             scope: compute fused with send, no copy kernel.  Off
+ *             under the ablations and the transport negative controls.  Bitwise identical results.
+ *  "pair_recompute" 1 (default) = F'_{i-1,j} runs on a second lane beside B_{i,j}, both stream
+ *             tasks on half grids (F' depends only on the stage input); 0 = in place.
  * Table 1 ablation toggles (results are bitwise those of the default -- only the
  * issue order and the copy path change).  Need every partition in this process, and not between
  * forward and backward (TGP_E_UNSUPPORTED / TGP_E_STATE):

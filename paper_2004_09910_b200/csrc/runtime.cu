@@ -305,6 +305,20 @@ static int st_build_desc(tgp_ctx* c, Stage& s, int B) {
 
 static bool use_stream(const tgp_ctx* c, const Stage& s, int M) { return s.st_ok && c->stream && M <= 16; }
 
+// Compute fused with send: a stream-kernel task writes its boundary tensor straight
+// into the neighbour's receive slab and release-stores the flag itself, so the copy record has no
+// kernel.  Off under the Table 1 ablations and the transport negative controls (they act on the copy).
+static bool send_ok(const tgp_ctx* c) {
+  return c->fused_send && !c->abl_streams && !c->relay && c->order_seed == 0 && c->drop_push_part < 0 &&
+         c->delay_push_ns == 0 && c->skip_wait_part < 0 && c->transport == 2;
+}
+static bool fuse_fwd(const tgp_ctx* c, const Stage& s, int M) {
+  return send_ok(c) && s.j + 1 < c->n && use_stream(c, s, M) && c->view[s.j + 1].fwd_in;
+}
+static bool fuse_bwd(const tgp_ctx* c, const Stage& s, int M) {
+  return send_ok(c) && s.j > 0 && use_stream(c, s, M) && c->view[s.j - 1].grad_in;
+}
+
 // LayerNorm folded into GEMM1 of the stream kernel: recompute c = W1 gamma, e = W1 beta + b1 of
 // every block after the weights or LN parameters changed (SGD step, set / init).
 static int st_refold(tgp_ctx* c, Stage& s, int B) {
@@ -319,7 +333,8 @@ static int st_refold(tgp_ctx* c, Stage& s, int B) {
 
 // lane: 0 = full grid on comp; 1 = half grid on comp (a paired B); 2 = half grid on comp2 with the
 // lane-1 counters / statistics (a paired F', beside the lane-1 B)
-static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd, int lane = 0) {
+static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd, int lane = 0, float* send_to = nullptr,
+                            uint32_t* send_flag = nullptr) {
   const LayerRT& L0 = c->layers[s.l0];
   STask t{};
   t.L = s.l1 - s.l0;
@@ -333,6 +348,12 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
   t.nv = lane ? 2 : 1;
   t.gy_top = s.self.grad_in + (size_t)r0 * s.d_out;
   t.dx_bottom = s.dx_out + (size_t)r0 * s.d_in;
+  // fused send (f3): forward -> the last block writes the consumer's receive slab; backward -> the
+  // input gradient goes to the producer partition's gradient slab
+  if (send_to && bwd) t.dx_bottom = send_to;
+  t.y_send = (send_to && !bwd) ? send_to : nullptr;
+  t.send_flag = send_to ? send_flag : nullptr;
+  t.send_seq = s.dseq;
   t.gbuf0 = s.gbuf[0];
   t.gbuf1 = s.gbuf[1];
   t.stats = lane == 2 ? s.st_stats2 : s.st_stats;
@@ -876,10 +897,10 @@ static int exec_wgrad(tgp_ctx* c, Stage& s, int B, bool fused = false) {
 // Each task's kernel sequence is captured once into a CUDA graph (per micro-batch, per batch size)
 // and replayed: one host launch per task instead of ~3 per layer.
 template <typename Fn>
-static int run_task(tgp_ctx* c, Stage& s, TaskGraph& tg, int B, Fn&& fn, cudaStream_t st = nullptr) {
+static int run_task(tgp_ctx* c, Stage& s, TaskGraph& tg, int B, Fn&& fn, cudaStream_t st = nullptr, int mode = 0) {
   if (!st) st = s.comp;
   if (!c->use_graphs) return fn();
-  if (tg.exec && tg.B == B) {
+  if (tg.exec && tg.B == B && tg.mode == mode) {
     TGP_CUDA_TRY(cudaGraphLaunch(tg.exec, st));
     c->kernels += tg.kernels;
     return 0;
@@ -902,6 +923,7 @@ static int run_task(tgp_ctx* c, Stage& s, TaskGraph& tg, int B, Fn&& fn, cudaStr
   cudaGraphDestroy(graph);
   TGP_CUDA_TRY(ce);
   tg.B = B;
+  tg.mode = mode;
   tg.kernels = c->kernels - k0;
   c->kernels = k0;
   TGP_CUDA_TRY(cudaGraphLaunch(tg.exec, st));
@@ -1008,6 +1030,13 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       if (!sp) return 0;  // actor is the source; remote source -> nothing to issue here
       Stage& s = *sp;
       const bool skip = rc.kind == K_SKIP_F || rc.kind == K_SKIP_B;
+      if ((rc.kind == K_COPY_F && fuse_fwd(c, s, M)) || (rc.kind == K_COPY_B && fuse_bwd(c, s, M))) {
+        // fused with the producing task (f3): the task kernel wrote the consumer's slab and flag
+        c->copy_bytes += (int64_t)M * (rc.kind == K_COPY_F ? s.d_out : s.d_in) * 4;
+        c->copy_msgs++;
+        c->issue_log.push_back(rc);
+        return 0;
+      }
       cudaStream_t st = skip ? s.cskip : s.cact;
       cudaEvent_t ev = (rc.kind == K_COPY_F || rc.kind == K_SKIP_F) ? s.fdone[i - 1] : s.bdone[i - 1];
       if (c->abl_streams) {
@@ -1143,16 +1172,41 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       }
       if (rc.kind == K_B && s.pair_ok && s.hoisted[i] == 1) TGP_CUDA_TRY(cudaStreamWaitEvent(s.comp, s.rdone[i - 1], 0));
       if (rc.kind == K_RECOMPUTE && s.pair_ok) s.hoisted[i] = 2;  // issued in place
+      // fused send: the task writes the neighbour's receive slab, which the neighbour must have
+      // finished using in the previous call (R2; the push path does this wait on its copy stream)
+      const bool send = (rc.kind == K_F && fuse_fwd(c, s, M)) || (rc.kind == K_B && fuse_bwd(c, s, M));
+      const int nb = rc.kind == K_B ? j - 1 : j + 1;
+      if (send && !first_push[j][nb]) {
+        TGP_TRY(wait_flag(c, s.comp, flag_done(c, s.self, nb), seq - 1));
+        first_push[j][nb] = 1;
+      }
+      float* send_to = nullptr;
+      uint32_t* send_flag = nullptr;
+      if (send && rc.kind == K_F) {
+        send_to = c->view[nb].fwd_in + (size_t)r0 * s.d_out;
+        send_flag = flag_fwd(c->view[nb], i);
+      } else if (send) {
+        send_to = c->view[nb].grad_in + (size_t)r0 * s.d_in;
+        send_flag = flag_grad(c, c->view[nb], i);
+      }
       cudaEvent_t ta = nullptr;
       trace_begin(c, s, s.comp, 0, rc.kind, i, &ta);
-      if (rc.kind == K_B && paired) {
-        TGP_TRY(run_task(c, s, s.gB2[i - 1], B, [&] { return exec_task_stream(c, s, i, r0, M, true, 1); }));
+      if (rc.kind == K_B && (paired || send)) {
+        TGP_TRY(run_task(c, s, paired ? s.gB2[i - 1] : s.gB[i - 1], B,
+                         [&] { return exec_task_stream(c, s, i, r0, M, true, paired ? 1 : 0, send_to, send_flag); },
+                         nullptr, send ? 1 : 0));
         TGP_CUDA_TRY(cudaEventRecord(s.bdone[i - 1], s.comp));
       } else if (rc.kind == K_B) {
         TGP_TRY(run_task(c, s, s.gB[i - 1], B, [&] { return exec_backward(c, s, i, r0, M); }));
         TGP_CUDA_TRY(cudaEventRecord(s.bdone[i - 1], s.comp));
+      } else if (send) {  // F_{i,j} sending its output
+        TGP_TRY(run_task(c, s, s.gF[i - 1], B,
+                         [&] { return exec_task_stream(c, s, i, r0, M, false, 0, send_to, send_flag); }, nullptr, 1));
+        TGP_CUDA_TRY(cudaEventRecord(s.fdone[i - 1], s.comp));
       } else {
-        TGP_TRY(run_task(c, s, s.gF[i - 1], B, [&] { return exec_forward(c, s, i, r0, M); }));
+        // F without a send, or F' (never sends; with a sending F it has its own graph)
+        TaskGraph& tg = (rc.kind == K_RECOMPUTE && fuse_fwd(c, s, M)) ? s.gR[i - 1] : s.gF[i - 1];
+        TGP_TRY(run_task(c, s, tg, B, [&] { return exec_forward(c, s, i, r0, M); }));
         if (rc.kind == K_F) TGP_CUDA_TRY(cudaEventRecord(s.fdone[i - 1], s.comp));
       }
       trace_end(c, s, s.comp, 0, rc.kind, i, ta);
@@ -1286,6 +1340,11 @@ static int begin_call(tgp_ctx* c) {
   c->seq++;
   for (Stage* s : c->local)
     if (s) s->abl_next = 0;
+  for (Stage* s : c->local)
+    if (s) {  // the fused-send flags carry the call's sequence number (read on the device)
+      TGP_CUDA_TRY(cudaSetDevice(s->dev));
+      TGP_CUDA_TRY(cudaMemcpyAsync(s->dseq, &c->seq, 4, cudaMemcpyHostToDevice, s->comp));
+    }
   for (int j = 0; j < c->n; ++j) {
     Stage* sp = c->local[j];
     if (!sp) continue;

@@ -70,6 +70,7 @@ struct LayerRT {
 struct TaskGraph {
   cudaGraphExec_t exec = nullptr;
   int B = -1;
+  int mode = 0;  // what else the captured kernels bake in (fused send on / off)
   int64_t kernels = 0;
 };
 
@@ -137,6 +138,8 @@ struct Stage {
   std::vector<cudaEvent_t> rdone;     // per micro-batch: its hoisted F' finished (recorded on comp2)
   std::vector<char> hoisted;          // per micro-batch: F' already issued on lane 1 in this call
   std::vector<TaskGraph> gR2, gB2;    // paired-task graphs (half grid)
+  std::vector<TaskGraph> gR;          // F' graphs when F sends fused (F and F' differ then)
+  uint32_t* dseq = nullptr;           // device copy of the call sequence number (fused-send flags)
   unsigned long long* st_dbg = nullptr;  // diagnostics (TGP_ST_DEBUG): [grid][2L][ST_DBG_SLOTS]
   cudaEvent_t* prof_ev = nullptr;  // tgp_profile_layers: per-layer boundary events (forward, then backward)
   void* red_items = nullptr;  // device RedItem[n_red]: column-partial -> gradient reductions of W_j
@@ -192,6 +195,7 @@ struct tgp_ctx {
   bool l2pf = false;
   bool stream = true;
   bool pair = true;           // F'_{i-1,j} beside B_{i,j} on half grids (option "pair_recompute")
+  bool fused_send = true;     // stream-kernel tasks store their boundary tensor into the consumer's slab (option "fused_send")
   bool pair_slots = false;    // checkpointed micro-batches alternate two scratch slots (set at create)
   bool gemm_wide = true;      // per-micro-batch GEMMs with >= 256 rows through the persistent gemm_wide kernel (option "gemm_wide")
   bool dw_persistent = true;  // deferred dW through the persistent gemm_dw kernel (option "dw_persistent")

@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
           const bool more = l + 1 < t.L;
           const float gnext = more ? t.layers[l + 1].gamma[fo] : 0.0f;
           __nv_bfloat16* const yg = Ly.yg;
-          float* const yout = Mi.y;
+          float* const yout = (t.y_send && l + 1 == t.L) ? t.y_send : Mi.y;  // fused send: the consumer's slab
           float acc[4];
           gemm_result(std::integral_constant<int, 16>{}, acc, nullptr);
 #pragma unroll
@@ -922,13 +922,25 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
   unsigned* done = t.cnt + (size_t)ncnt * CNT_STRIDE;
   __shared__ int last;
   if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(done, 1u) == gridDim.x - 1;
+    unsigned prev;
+    if (t.send_flag) {
+      // fused send: this CTA's stores into the consumer's receive slab (ordered before this thread by
+      // the barrier above) become visible at system scope before its arrival is counted
+      asm volatile("atom.add.acq_rel.sys.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(done) : "memory");
+    } else {
+      __threadfence();
+      prev = atomicAdd(done, 1u);
+    }
+    last = prev == gridDim.x - 1;
   }
   __syncthreads();
   if (last) {
     for (int k = threadIdx.x; k < ncnt; k += blockDim.x) t.cnt[(size_t)k * CNT_STRIDE] = 0u;
-    if (threadIdx.x == 0) *done = 0u;
+    if (threadIdx.x == 0) {
+      *done = 0u;
+      if (t.send_flag)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(t.send_flag), "r"(*t.send_seq) : "memory");
+    }
   }
 }
 

@@ -64,6 +64,14 @@ struct STask {
   // diagnostics only (nullptr on the product path): per CTA and phase, %globaltimer stamps
   // [grid][2L][ST_DBG_SLOTS] (TGP_ST_DEBUG); they do not change any result
   unsigned long long* dbg;
+  // compute fused with send: the task's boundary tensor --
+  // forward: the last block's output rows, y_send; backward: the input-gradient rows, dx_bottom -- is
+  // stored straight into the consuming partition's receive slab (same device, peer or CUDA-IPC
+  // mapping), and the last CTA to finish release-stores *send_seq into send_flag at system scope
+  // (every CTA first makes its stores visible with a system-scope acq_rel atomic).  nullptr: no send.
+  float* y_send;
+  uint32_t* send_flag;
+  const uint32_t* send_seq;  // device copy of the call sequence number (graph replays read it)
   unsigned sleep_ns;  // back-off between dependency polls
   unsigned inflight;  // max weight tiles issued but not landed per CTA (0 = limited by the ring only)
 };

@@ -31,7 +31,7 @@ def test_device_order_and_copy_overlap(tmp_path):
     x, t, params = make_case(layers, 64, 2, "bf16")
     # the paper's per-device order, without F' / B pairing (pairing is checked in test_gpu_pairing.py)
     g, P = gpu_step(layers, params, x, t, m=m, n=n, ckpt="except_last", dtype="bf16", lr=0.05,
-                    options={"graphs": 1, "pair_recompute": 0}, steps=1)
+                    options={"graphs": 1, "pair_recompute": 0, "fused_send": 0}, steps=1)
     # a second, traced step
     import torch
     P.set_trace(True)
