@@ -63,6 +63,12 @@ typedef enum { TGP_FP32 = 0, TGP_BF16 = 1 } tgp_dtype;
  *  TGP_BATCHNORM y = act(gamma (x - mu_i) / sqrt(var_i + 1e-5) + beta), statistics of micro-batch i
  *                (P:56 footnote); running stats committed once per forward call from the whole
  *                mini-batch (momentum 0.1, unbiased variance).   gamma [d], beta [d]   (FP32 mode only)
+ *  TGP_LAYERNORM y = gamma (x - mu) / sqrt(var + 1e-5) + beta over the features of each row (biased
+ *                variance), d_out == d_in, act none, no dropout.   gamma [d], beta [d]
+ *  TGP_DROPOUT   y = x * keep / (1 - p), p = `dropout`, keep from Philox at site = layer index (the
+ *                same counters as every other dropout site), d_out == d_in, act none; no parameters.
+ *                (a partition is any sequence of layers; P:105 / P:212: the recompute
+ *                regenerates the same mask from the restored RNG state.)
  *
  * GPT-2-shaped kinds (C5; BASELINE.json configs[4]; bf16 mode only).  Rows are TOKENS:
  * a sample is a sequence of `seq` tokens, B counts tokens and must be a multiple of seq, and the
@@ -86,7 +92,9 @@ typedef enum {
   TGP_BATCHNORM = 3,
   TGP_EMBED = 4,
   TGP_TRANSFORMER = 5,
-  TGP_LMHEAD = 6
+  TGP_LMHEAD = 6,
+  TGP_LAYERNORM = 7,
+  TGP_DROPOUT = 8
 } tgp_kind;
 typedef enum { TGP_ACT_NONE = 0, TGP_ACT_RELU = 1, TGP_ACT_GELU = 2 } tgp_act;
 

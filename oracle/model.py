@@ -72,7 +72,7 @@ def act_df(name, z):
 
 def n_params(L):
     return {"linear": 2, "merge": 2, "resmlp": 6, "batchnorm": 2, "embed": 2, "transformer": 12,
-            "lmhead": 3}[L["kind"]]
+            "lmhead": 3, "layernorm": 2, "dropout": 0}[L["kind"]]
 
 
 def row_unit(layers):
@@ -231,6 +231,13 @@ def layer_fwd(L, p, x, s, *, site, seed, step, row0, groups):
         gamma, beta, W = p
         h, c = _ln_fwd(x, gamma, beta)
         return h @ W.T, (h, c)
+    if k == "layernorm":  # standalone LayerNorm over the features of each row ("a sequence of layers")
+        gamma, beta = p
+        h, c = _ln_fwd(x, gamma, beta)
+        return h, c
+    if k == "dropout":  # standalone dropout: Philox mask of this layer's site (reading Z17)
+        y, keep = _drop(x, pdrop, seed, step, site, row0)
+        return y, keep
     if k == "batchnorm":
         gamma, beta = p
         y = np.empty_like(x)
@@ -311,6 +318,12 @@ def layer_bwd(L, p, cache, dy, *, groups):
         h, c = cache
         dx, dg, db = _ln_bwd(dy @ W, gamma, c)
         return dx, None, [dg, db, dy.T @ h]
+    if k == "layernorm":
+        gamma, beta = p
+        dx, dg, db = _ln_bwd(dy, gamma, cache)
+        return dx, None, [dg, db]
+    if k == "dropout":
+        return _undrop(dy, cache, pdrop), None, []
     if k == "batchnorm":
         gamma, beta = p
         dx = np.empty_like(dy)

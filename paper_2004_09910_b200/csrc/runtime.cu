@@ -559,6 +559,24 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
                          nullptr, false, d, M, H, r0, H, true, e4));
         break;
       }
+      case TGP_LAYERNORM:
+      case TGP_DROPOUT: {
+        if (L.L.kind == TGP_LAYERNORM) {
+          TGP_TRY(ln_fwd(s.comp, pdl() && c->use_pdl, x, din, M, din, mparam(s, L, 0), mparam(s, L, 1), y, dout, false,
+                         L.mean[slot], L.rstd[slot]));
+        } else {  // y = x * keep / (1 - p): the Philox mask of site l (colwise, no activation)
+          const float p = L.L.dropout;
+          TGP_TRY(colwise(s.comp, pdl() && c->use_pdl, x, din, nullptr, M, din, 0, drop_thresh(p),
+                          p > 0 ? 1.0f / (1.0f - p) : 1.0f, c->seed, s.dstep, (uint32_t)l, r0, y, dout, false, nullptr));
+        }
+        c->kernels++;
+        if (L.L.stash_route >= 0) {
+          TGP_TRY(convert_rows(s.comp, false, y, dout, M, dout, stash_dst(c, s, L.L.stash_route, r0), dout, c->bf16,
+                               nullptr));
+          c->kernels++;
+        }
+        break;
+      }
       case TGP_BATCHNORM: {
         const size_t so = (size_t)(i - 1) * din;
         TGP_TRY(bn_fwd(s.comp, x, M, din, mparam(s, L, 0), mparam(s, L, 1), L.L.act, y, L.z[slot], L.bn_mu + so,
@@ -761,6 +779,21 @@ static int exec_backward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
         dyop_ready = false;
         break;
       }
+      case TGP_LAYERNORM: {
+        // dx = LN_bwd(dy) with the per-16-row dgamma / dbeta column partials of micro-batch i
+        TGP_TRY(ln_bwd_any(c, s, pdl() && c->use_pdl, g, xin, L.mean[slot], L.rstd[slot], mparam(s, L, 0), nullptr, dx,
+                           M, din, L.pg + po * din, L.pbt + po * din));
+        dyop_ready = false;
+        break;
+      }
+      case TGP_DROPOUT: {  // dx = dy * keep / (1 - p), the same mask (same site, counters and step)
+        const float p = L.L.dropout;
+        TGP_TRY(colwise(s.comp, pdl() && c->use_pdl, g, dout, nullptr, M, dout, 0, drop_thresh(p),
+                        p > 0 ? 1.0f / (1.0f - p) : 1.0f, c->seed, s.dstep, (uint32_t)l, r0, dx, din, false, nullptr));
+        c->kernels++;
+        dyop_ready = false;
+        break;
+      }
       case TGP_BATCHNORM: {
         TGP_TRY(bn_bwd(s.comp, g, xin, L.z[slot], L.bn_mu + pbn * din, L.bn_rstd + pbn * din, mparam(s, L, 0), M, din,
                        L.L.act, dx, L.pg + po * din, L.pb + po * din));
@@ -873,6 +906,8 @@ static int exec_wgrad(tgp_ctx* c, Stage& s, int B, bool fused = false) {
         break;
       }
       case TGP_BATCHNORM:
+      case TGP_LAYERNORM:
+      case TGP_DROPOUT:
         break;
     }
   }

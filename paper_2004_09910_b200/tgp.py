@@ -13,7 +13,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TGP_LIB") or os.path.join(_HERE, "libtgp.so")
 
-KIND = {"linear": 0, "resmlp": 1, "merge": 2, "batchnorm": 3, "embed": 4, "transformer": 5, "lmhead": 6}
+KIND = {"linear": 0, "resmlp": 1, "merge": 2, "batchnorm": 3, "embed": 4, "transformer": 5, "lmhead": 6,
+        "layernorm": 7, "dropout": 8}
 ACT = {"none": 0, "relu": 1, "gelu": 2}
 CKPT = {"always": 0, "except_last": 1, "never": 2}
 DTYPE = {"fp32": 0, "bf16": 1}

@@ -102,6 +102,15 @@ def C5(n=8, m=32, checkpoint="always", batch=32, n_layers=48):
                   lr=0.01)
 
 
+def ln_mlp(n_blocks=2, d=256, dropout=0.1):
+    """A sequence of plain layers with the standalone LayerNorm and Dropout kinds (any
+    sequence of layers): n_blocks x [Linear(d->d, GELU), LayerNorm(d), Dropout(p)], Linear(d->d)."""
+    out = []
+    for _ in range(n_blocks):
+        out += [layer("linear", d, d, act="gelu"), layer("layernorm", d, d), layer("dropout", d, d, dropout=dropout)]
+    return out + [layer("linear", d, d)]
+
+
 def bn_mlp(n=4, d=256):
     """BN micro-config: n x [Linear(d->d), BatchNorm(d), ReLU]."""
     L = []
@@ -141,7 +150,8 @@ def param_shapes(layers):
     linear:    W [d_out, d_in], b [d_out]
     merge:     W [d_out, d_in + d_skip], b [d_out]
     resmlp:    gamma [d_in], beta [d_in], W1 [d_hidden, d_in], b1 [d_hidden], W2 [d_out, d_hidden], b2 [d_out]
-    batchnorm: gamma [d], beta [d]
+    batchnorm, layernorm: gamma [d], beta [d]
+    dropout:   (no parameters)
     Returns a list of (layer_index, name, shape).
     """
     out = []
@@ -155,8 +165,10 @@ def param_shapes(layers):
             d, h = L["d_in"], L["d_hidden"]
             out += [(li, "gamma", (d,)), (li, "beta", (d,)), (li, "W1", (h, d)), (li, "b1", (h,)),
                     (li, "W2", (L["d_out"], h)), (li, "b2", (L["d_out"],))]
-        elif k == "batchnorm":
+        elif k in ("batchnorm", "layernorm"):
             out += [(li, "gamma", (L["d_in"],)), (li, "beta", (L["d_in"],))]
+        elif k == "dropout":
+            pass
         elif k == "embed":
             out += [(li, "wte", (L["vocab"], L["d_out"])), (li, "wpe", (L["seq"], L["d_out"]))]
         elif k == "transformer":

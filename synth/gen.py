@@ -51,11 +51,16 @@ def inputs(layers, batch, seed=1234, dtype="fp32", x_mean=0.0):
     return x, t
 
 
-def params(layers, seed=1234, dtype="fp32", ln="default"):
+def params(layers, seed=1234, dtype="fp32", ln="default", only=None):
     """Return the list of float32 parameter arrays in canonical order (configs.param_shapes).
-    ln = "default" (gamma ~ 1 + 0.1 N, beta ~ 0.1 N) or "wide" (gamma ~ U(0.25, 4), beta ~ N(0, 1))."""
+    ln = "default" (gamma ~ 1 + 0.1 N, beta ~ 0.1 N) or "wide" (gamma ~ U(0.25, 4), beta ~ N(0, 1)).
+    only: optional set of parameter indices to generate (None in the other slots; every tensor has
+    its own seeded stream, so a subset is identical to the same entries of the full list)."""
     out = []
     for pid, (li, name, shape) in enumerate(param_shapes(layers)):
+        if only is not None and pid not in only:
+            out.append(None)
+            continue
         g = rng(seed, TID_PARAM0 + pid)
         if name in ("wte", "wpe"):
             a = g.standard_normal(shape)

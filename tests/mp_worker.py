@@ -33,15 +33,24 @@ def main():
     elif cfg == "gpt2":
         layers = C.gpt2_stack(3, 128, 2, 64, 512, 0.1)  # embed + 3 blocks + LM head
         bal = {2: [2, 3], 3: [2, 2, 1]}[ws]
+    elif cfg == "c2n8":
+        # the BASELINE C2 model at n = 8: 32 x RESMLP(4096), 4 blocks per rank, B = 512, m = 32
+        layers = C.resmlp_stack(32, 4096)
+        bal = [32 // ws] * ws
     else:
         # "stream": d = 512, eligible for the persistent stream kernel in every partition
         layers = C.resmlp_stack(2 * ws, 512 if cfg == "stream" else 256, dropout=0.1)
         bal = [2] * ws
     B, m, lr, seed = (64 if cfg == "stream" else 32), 4, 0.05, 11
+    if cfg == "c2n8":
+        B, m = 512, 32
     x, t = G.inputs(layers, 4 if cfg == "gpt2" else B, seed=seed, dtype="bf16")
     if cfg == "gpt2":
         B, m = x.shape[0], 2  # 4 sequences of 64 tokens, 2 micro-batches
-    params = G.params(layers, seed=seed, dtype="bf16")
+    own = None
+    if cfg == "c2n8":  # generate only this rank's parameters (1.07 B in all)
+        own = set(range(6 * (32 // ws) * rank, 6 * (32 // ws) * (rank + 1)))
+    params = G.params(layers, seed=seed, dtype="bf16", only=own)
     devices = [-1] * ws
     devices[rank] = dev
     P = Pipeline(layers, chunks=m, devices=devices, balance=bal, checkpoint="except_last", max_batch=B,
@@ -69,8 +78,9 @@ def main():
         if first:
             res[f"dx{step}"] = DX.cpu().numpy()
         for i in range(P.n_params):
-            if P.param_info(i)[1] == rank:
-                res[f"g{step}_{i}"] = P.get_grad(i)
+            if P.param_info(i)[1] == rank and (cfg != "c2n8" or step == 0):
+                g = P.get_grad(i)
+                res[f"g{step}_{i}"] = g[::97] if cfg == "c2n8" else g  # c2n8: a fixed subsample
         P.step(lr)
     res["log"] = P.issue_log()
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **res)

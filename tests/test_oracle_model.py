@@ -35,6 +35,10 @@ def tiny_umlp(d=6):
     return C.umlp(d=d, levels=2, blocks_per_level=1, mid_blocks=1)
 
 
+def tiny_ln(d=7):
+    return C.ln_mlp(2, d, dropout=0.3)
+
+
 def tiny_bn(d=5):
     return [C.layer("linear", d, d), C.layer("batchnorm", d, d, act="relu"),
             C.layer("linear", d, d), C.layer("batchnorm", d, d, act="none")]
@@ -45,7 +49,7 @@ def _loss(layers, params, x, t, m, seed, step):
     return M.mse(y, t)[0]
 
 
-@pytest.mark.parametrize("mk,m", [(tiny_resmlp, 1), (tiny_umlp, 1), (tiny_bn, 2)])
+@pytest.mark.parametrize("mk,m", [(tiny_resmlp, 1), (tiny_umlp, 1), (tiny_bn, 2), (tiny_ln, 2)])
 def test_finite_differences(mk, m):
     layers = mk()
     x, t = G.inputs(layers, 4, seed=11)
@@ -111,6 +115,13 @@ def torch_step(layers, params, x, t, m, seed, step, lr=None):
                 keep = torch.tensor(dropout_keep(seed, step, li, 0, B, g.shape[1], L["dropout"]))
                 g = g * keep / (1 - L["dropout"])
             y = h + torch.nn.functional.linear(g, W2, b2)
+        elif L["kind"] == "layernorm":
+            g_, b_ = P[k:k + 2]
+            k += 2
+            y = torch.nn.functional.layer_norm(h, (h.shape[1],), g_, b_, eps=1e-5)
+        elif L["kind"] == "dropout":
+            keep = torch.tensor(dropout_keep(seed, step, li, 0, B, h.shape[1], L["dropout"]))
+            y = h * keep / (1 - L["dropout"])
         elif L["kind"] == "batchnorm":
             g_, b_ = P[k:k + 2]
             k += 2
@@ -137,7 +148,7 @@ def torch_step(layers, params, x, t, m, seed, step, lr=None):
     return float(loss.detach()), grads, X.grad.numpy(), running, [p.detach().numpy() for p in P]
 
 
-@pytest.mark.parametrize("name", ["C1", "C2small", "C2small_drop", "C4small", "BN"])
+@pytest.mark.parametrize("name", ["C1", "C2small", "C2small_drop", "C4small", "BN", "LN"])
 def test_vs_torch_autograd(name):
     if name == "C1":
         cfg = C.C1()
@@ -148,6 +159,8 @@ def test_vs_torch_autograd(name):
         layers, B, m = C.resmlp_stack(4, 128, dropout=0.1), 32, 1
     elif name == "C4small":
         layers, B, m = C.umlp(d=64), 16, 1
+    elif name == "LN":
+        layers, B, m = C.ln_mlp(3, 64, dropout=0.2), 24, 3
     else:
         cfg = C.BN()
         layers, B, m = cfg.layers, cfg.batch, cfg.m
