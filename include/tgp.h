@@ -121,6 +121,12 @@ typedef struct tgp_ctx tgp_ctx;
  * sum, ties broken by the lexicographically smallest boundary vector.  balance_out[n_parts]. */
 tgp_status tgp_balance(const double* layer_cost, int32_t n_layers, int32_t n_parts, int32_t* balance_out);
 
+/* Size-based per-layer cost for tgp_balance (§4.2.2 P:312-317 "parameters consume 8 bytes
+ * each for itself and its gradients"; SPEC profile_size): bytes_out[l] = 8 x (parameter count of
+ * layer l) + rows x d_out x 4 (the fp32 activation output of a `rows`-row sample).  A MERGE layer's
+ * skip width is taken from the layer that stashes its route.  Pure host; rows >= 1. */
+tgp_status tgp_profile_size(const tgp_layer* layers, int32_t n_layers, int32_t rows, double* bytes_out);
+
 /* Micro-batch split (reading Z7): sizes_out[m] = ceil(B/m) for the first B mod m
  * micro-batches, floor(B/m) after.  TGP_E_INVALID unless 1 <= m <= B. */
 tgp_status tgp_split(int32_t B, int32_t m, int32_t* sizes_out);
@@ -311,8 +317,10 @@ tgp_status tgp_memory(tgp_ctx* ctx, int32_t part, int64_t* used, int64_t* reserv
  * bytes of the bf16 dW-operand and skip stash: rows of the WHOLE mini-batch, kept from F until W_j,
  * allocated in every checkpoint mode (deferred dW) -- checkpointing does NOT shrink it.
  * *slots = bytes of the per-activation-slot fp32 buffers (layer outputs, pre-activations, LayerNorm
- * statistics); *n_slots = slot count: 1 shared scratch + one per non-checkpointed micro-batch, i.e.
- * m + 1 (never), 2 (except_last), 1 (always).  Only the slots are what checkpointing saves here.  Both
+ * statistics); *n_slots = slot count: the shared scratch slot(s) + one per non-checkpointed
+ * micro-batch, i.e. m + 1 (never), 2 (except_last), 1 (always) -- one scratch slot more when F' / B
+ * pairing is possible (stream-kernel shapes, >= 2 checkpointed micro-batches: alternating scratch
+ * slots).  Only the slots are what checkpointing saves here.  Both
  * byte counts are included in tgp_memory's *used.  Any pointer may be NULL. */
 tgp_status tgp_memory_breakdown(tgp_ctx* ctx, int32_t part, int64_t* stash, int64_t* slots, int32_t* n_slots);
 

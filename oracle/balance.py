@@ -55,3 +55,17 @@ def block_max(costs, sizes):
         out.append(sum(costs[e:e + s]))
         e += s
     return max(out)
+
+
+def profile_size(layers, rows):
+    """SPEC profile_size (§4.2.2: "parameters consume 8 bytes each for itself and
+    its gradients"): per layer, 8 x its parameter count + the activation output of a `rows`-row
+    sample in fp32 (rows x d_out x 4 bytes)."""
+    from synth.configs import param_shapes
+    import numpy as np
+    shapes = param_shapes(layers)
+    out = []
+    for li, L in enumerate(layers):
+        n = sum(int(np.prod(sh)) for (l, _, sh) in shapes if l == li)
+        out.append(8.0 * n + rows * L["d_out"] * 4.0)
+    return out

@@ -32,9 +32,15 @@ namespace tgp {
 namespace {
 constexpr int WS_BM = 128, WS_BN = 128, WS_BK = 64;
 constexpr int WS_STAGE = (WS_BM + WS_BN) * WS_BK * 2;  // 32 KB of operands per k-block
-constexpr int WS_STAGES = 3;
+#ifndef TGP_WS_STAGES
+#define TGP_WS_STAGES 3
+#endif
+#ifndef TGP_WS_NM
+#define TGP_WS_NM 5
+#endif
+constexpr int WS_STAGES = TGP_WS_STAGES;
 constexpr int WS_MCHUNK = 128 * 32 * 4;                // 16 KB master chunk (128 rows x 32 fp32)
-constexpr int WS_NM = 5;                               // master chunk ring
+constexpr int WS_NM = TGP_WS_NM;                       // master chunk ring
 constexpr int WS_SCHUNK = 128 * 64 * 2;                // 16 KB shadow chunk (128 rows x 64 bf16)
 constexpr int WS_OFF_M = WS_STAGES * WS_STAGE;
 constexpr int WS_OFF_S = WS_OFF_M + WS_NM * WS_MCHUNK;

@@ -1411,6 +1411,38 @@ tgp_status tgp_balance(const double* cost, int32_t L, int32_t n, int32_t* out) {
   return TGP_OK;
 }
 
+tgp_status tgp_profile_size(const tgp_layer* layers, int32_t L, int32_t rows, double* out) {
+  if (!layers || !out || L < 1 || rows < 1) {
+    set_error("tgp_profile_size: need layers, n_layers >= 1, rows >= 1");
+    return TGP_E_INVALID;
+  }
+  for (int l = 0; l < L; ++l) {
+    const tgp_layer& x = layers[l];
+    const double di = x.d_in, dout = x.d_out, H = x.d_hidden;
+    double skip = 0.0;
+    if (x.kind == TGP_MERGE)
+      for (int q = 0; q < L; ++q)
+        if (layers[q].stash_route >= 0 && layers[q].stash_route == x.pop_route) skip = layers[q].d_out;
+    double params = 0.0;
+    switch (x.kind) {
+      case TGP_LINEAR: params = dout * di + dout; break;
+      case TGP_MERGE: params = dout * (di + skip) + dout; break;
+      case TGP_RESMLP: params = 2 * di + H * di + H + dout * H + dout; break;
+      case TGP_BATCHNORM:
+      case TGP_LAYERNORM: params = 2 * di; break;
+      case TGP_DROPOUT: params = 0.0; break;
+      case TGP_EMBED: params = ((double)x.vocab + x.seq) * dout; break;
+      case TGP_TRANSFORMER: params = 2 * di + 3 * di * di + 3 * di + di * di + di + 2 * di + H * di + H + di * H + di; break;
+      case TGP_LMHEAD: params = 2 * di + dout * di; break;
+      default:
+        set_error("tgp_profile_size: layer %d has unknown kind %d", l, x.kind);
+        return TGP_E_INVALID;
+    }
+    out[l] = 8.0 * params + (double)rows * dout * 4.0;
+  }
+  return TGP_OK;
+}
+
 tgp_status tgp_split(int32_t B, int32_t m, int32_t* sizes) {
   if (!sizes || m < 1 || m > B) {
     set_error("tgp_split: need 1 <= m <= B (m=%d B=%d)", m, B);

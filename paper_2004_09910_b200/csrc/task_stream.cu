@@ -492,6 +492,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
     auto signal = [&](int id, int q) {
       if (et == 0 && q < 4) dbg_stamp(t, cur_p, 9);
       epi_bar();
+      if (et == 0 && q < 4) dbg_stamp(t, cur_p, 12);  // all 128 threads stored (barrier passed)
       if (et == 0) {
         // release: the epilogue barrier orders the other threads' stores before this reduction
         asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(cnt(id, q)), "r"(1u) : "memory");

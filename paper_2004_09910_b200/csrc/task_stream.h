@@ -75,7 +75,7 @@ struct STask {
   unsigned sleep_ns;  // back-off between dependency polls
   unsigned inflight;  // max weight tiles issued but not landed per CTA (0 = limited by the ring only)
 };
-constexpr int ST_DBG_SLOTS = 12;
+constexpr int ST_DBG_SLOTS = 13;
 
 int task_stream_smem();
 int task_stream_counter_bytes(int L);

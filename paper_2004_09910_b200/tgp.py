@@ -44,6 +44,7 @@ _I64 = ctypes.c_int64
 
 _SIGS = {
     "tgp_balance": [ctypes.POINTER(ctypes.c_double), _I32, _I32, ctypes.POINTER(_I32)],
+    "tgp_profile_size": [_P, _I32, _I32, ctypes.POINTER(ctypes.c_double)],
     "tgp_split": [_I32, _I32, ctypes.POINTER(_I32)],
     "tgp_schedule": [_I32, _I32, _I32, ctypes.POINTER(_I32), _I32, ctypes.POINTER(_I32), _I64,
                      ctypes.POINTER(_I64)],
@@ -137,6 +138,21 @@ def balance(costs, n):
     out = (_I32 * n)()
     _check(lib().tgp_balance(c, len(costs), n, out), "tgp_balance")
     return list(out)
+
+
+def profile_size(layers, rows):
+    """Per-layer bytes (tgp_profile_size): 8 x parameters + rows x d_out x 4 (§4.2.2)."""
+    arr = to_c_layers(layers)
+    out = (ctypes.c_double * len(layers))()
+    _check(lib().tgp_profile_size(arr, len(layers), rows, out), "tgp_profile_size")
+    return list(out)
+
+
+def balance_by_size(layers, n_parts, rows):
+    """Size-based partition (SPEC profile_size + blockpartition): min-max contiguous blocks of the
+    per-layer bytes.  Returns (balance, bytes)."""
+    sizes = profile_size(layers, rows)
+    return balance(sizes, n_parts), sizes
 
 
 def split(B, m):

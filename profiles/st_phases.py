@@ -39,9 +39,9 @@ L.tgp_debug_stream_read(P.h, 0, None, 0, ctypes.byref(n))
 buf = np.zeros(n.value, dtype=np.uint64)
 L.tgp_debug_stream_read(P.h, 0, buf.ctypes.data, n.value, ctypes.byref(n))
 NP = 2 * blocks
-G = n.value // (NP * 12)
-ev = buf.reshape(G, NP, 12).astype(np.int64)
-names = ["B issue", "W first", "W last", "B landed", "MMA done", "TMEM rdy", "partials", "signal", "stats", "sig entry", "MMA half", "cp last"]
+G = n.value // (NP * 13)
+ev = buf.reshape(G, NP, 13).astype(np.int64)
+names = ["B issue", "W first", "W last", "B landed", "MMA done", "TMEM rdy", "partials", "signal", "stats", "sig entry", "MMA half", "cp last", "bar passed"]
 t0 = ev[:, 0, 1].min()
 print(f"{'bwd' if bwd else 'fwd'} task, {blocks} blocks, {G} CTAs, ")
 prev = None

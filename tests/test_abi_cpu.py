@@ -140,3 +140,24 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp", ".inc")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), f
+
+
+def test_profile_size_matches_oracle_and_paper(L):
+    # SPEC profile_size / PAPER.md §4.2.2: 8 bytes per parameter (itself + its gradient) plus the
+    # fp32 activation output of the sample
+    from oracle import balance as OB
+    from synth import configs as C
+    # the SPEC example: linear 3 -> 2 with bias: 8 x (3*2 + 2) = 64 bytes + rows x 2 x 4
+    lin = [C.layer("linear", 3, 2)]
+    assert L.profile_size(lin, 5) == [64.0 + 5 * 2 * 4]
+    assert L.profile_size([C.layer("dropout", 8, 8, dropout=0.1)], 4) == [4 * 8 * 4.0]  # parameter-free
+    # doubling the rows doubles only the activation term
+    a, b = L.profile_size(lin, 5)[0], L.profile_size(lin, 10)[0]
+    assert b - a == 5 * 2 * 4
+    for layers in (C.mlp_chain(4, 64), C.resmlp_stack(4, 512, hidden=1024), C.umlp(d=128), C.ln_mlp(2, 64),
+                   C.gpt2_stack(2, 128, 2, 64, 512, 0.1), C.bn_mlp(2, 32)):
+        for rows in (1, 16, 512):
+            assert L.profile_size(layers, rows) == OB.profile_size(layers, rows)
+    # size balance of the C4 U-MLP: the merge layers (2d x d weights) weigh twice a plain linear
+    bal, sizes = L.balance_by_size(C.umlp(d=2048), 8, 8)
+    assert sum(bal) == len(C.umlp(d=2048)) and bal == OB.balance_dp(sizes, 8)
