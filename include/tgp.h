@@ -235,8 +235,10 @@ tgp_status tgp_get_bn_running(tgp_ctx* ctx, int32_t layer, float* mean, float* v
 tgp_status tgp_get_issue_log(tgp_ctx* ctx, int32_t* rec, int64_t cap, int64_t* n_rec);
 
 /* Task timeline (enabled by tgp_set_trace(ctx, 1)): per executed compute task and copy, 6 int64
- * (part, stream, kind, i, t0_ns, t1_ns), times from CUDA events relative to the start of the
- * call on that partition's device (not comparable across devices). */
+ * (part, stream, kind, i, t0_ns, t1_ns), times from CUDA events relative to the start of the last
+ * tgp_forward on that partition's device, so a forward and the backward after it share one time axis
+ * (not comparable across devices).  stream: 0 compute, 1 activation copies, 2 skip copies, 3 the
+ * second compute lane (F' paired beside B). */
 tgp_status tgp_set_trace(tgp_ctx* ctx, int32_t on);
 tgp_status tgp_get_timeline(tgp_ctx* ctx, int64_t* rec, int64_t cap, int64_t* n_rec);
 

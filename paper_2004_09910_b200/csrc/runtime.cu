@@ -1359,8 +1359,8 @@ static int finish_call(tgp_ctx* c) {
     for (auto& t : c->trace_recs) {
       Stage* s = c->local[t.part];
       float a = 0, b = 0;
-      cudaEventElapsedTime(&a, s->ev_start, t.a);
-      cudaEventElapsedTime(&b, s->ev_start, t.b);
+      cudaEventElapsedTime(&a, s->ev_epoch, t.a);
+      cudaEventElapsedTime(&b, s->ev_epoch, t.b);
       int64_t rec[6] = {t.part, t.stream, t.kind, t.i, (int64_t)(a * 1e6), (int64_t)(b * 1e6)};
       c->timeline.insert(c->timeline.end(), rec, rec + 6);
       cudaEventDestroy(t.a);

@@ -79,6 +79,7 @@ struct Stage {
   cudaStream_t comp = nullptr, cact = nullptr, cskip = nullptr;
   std::vector<cudaEvent_t> fdone, bdone;
   cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_epoch = nullptr;  // timeline origin: the start of the last tgp_forward on this partition
   std::vector<cudaEvent_t> tr_ev;  // timeline events (pairs)
   Pool pool;
   void* arena = nullptr;
