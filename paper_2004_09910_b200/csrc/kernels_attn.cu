@@ -521,6 +521,276 @@ __global__ void __launch_bounds__(256, TGP_ATTN_TC_MINB) attn_fwd_tc_kernel(Attn
   if (w == 0) tmem_dealloc(tmem, 256);
 }
 
+// ---------------------------------------------------------------- tcgen05 attention backward
+// The same VJP as attn_bwd_dkv_kernel / attn_bwd_dq_kernel (P recomputed from the saved log-sum-exp,
+// dS = Pd o (dPd - D), D = rowsum(dO o O); oracle/model.py _attn_bwd), on 128 x 128 tiles with every
+// product on the 5th-generation tensor cores: S = Q K^T and dP = dO V^T with the query as the MMA M
+// side (TMEM lane = query row), then the transposed products dV += Pd^T dO, dK += dS^T Q (dK/dV
+// kernel) or dQ += dS K (dQ kernel) read Pd / dS back from shared memory as MN-major operands, so no
+// transpose is ever materialised.  8 warps: warp w reads TMEM lane quadrant w & 3 and handles key
+// half w >> 2 of its query row (the forward's layout); one thread issues the MMAs.  Every output
+// element is accumulated by one CTA in a fixed order: deterministic.
+constexpr int BTC_SMEM_KV = 16384 * 8 + 64 + 1024;  // K, V, Q, dO, Pd (2 chunks), dS (2 chunks), barriers
+constexpr int BTC_SMEM_Q = 16384 * 6 + 64 + 1024;   // Q, dO, K, V, dS (2 chunks), barriers
+
+// fp32 [128][64] rows (row stride ld) -> bf16 SW128 tile (the K-major operand layout)
+TGP_DEV void load_sw_tile_f32(const float* g, int64_t ld, uint8_t* S) {
+  for (int q = threadIdx.x; q < TCQ * 8; q += blockDim.x) {
+    const int r = q >> 3, c = q & 7;
+    const float4 a = *reinterpret_cast<const float4*>(g + (int64_t)r * ld + c * 8);
+    const float4 b = *reinterpret_cast<const float4*>(g + (int64_t)r * ld + c * 8 + 4);
+    uint4 v;
+    v.x = pack2(a.x, a.y);
+    v.y = pack2(a.z, a.w);
+    v.z = pack2(b.x, b.y);
+    v.w = pack2(b.z, b.w);
+    *reinterpret_cast<uint4*>(S + sw_off(r, c)) = v;
+  }
+}
+
+// Pd and dS of this thread's 64 keys (half hf) of query row q for key tile kt, from the S and dP
+// accumulators in TMEM, written as bf16 into [128 q][128 k] tiles (two SW128 chunks of 64 keys).
+// Pd: the dropped-out probability (what dV sees); dS = P (dPd - D) with dPd the dropped-out dP.
+TGP_DEV void attn_bwd_tc_probs(const AttnArgs& A, uint32_t tS, uint32_t tdP, int row, int hf, int q, int kt,
+                               float lse_q, float D_q, uint64_t rowbase, uint32_t pstep, uint8_t* Pd, uint8_t* dS) {
+  const uint2 pkey = make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32));
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {  // 16 keys at a time
+    float sv[16], dv[16];
+    tmem_ld16(tS + hf * 64 + c * 16, sv);
+    tmem_ld16(tdP + hf * 64 + c * 16, dv);
+    float pv[16], gv[16];
+#pragma unroll
+    for (int g4 = 0; g4 < 4; ++g4) {
+      const int key0 = kt * TCQ + hf * 64 + c * 16 + 4 * g4;
+      uint32_t kb = 0xFu;
+      if (A.thresh) {
+        const uint64_t qi = (rowbase + (uint64_t)key0) >> 2;
+        const uint4 ph = philox4x32_10(make_uint4((uint32_t)qi, (uint32_t)(qi >> 32), A.site, pstep), pkey);
+        kb = ((ph.x >> 8) >= A.thresh ? 1u : 0u) | ((ph.y >> 8) >= A.thresh ? 2u : 0u) |
+             ((ph.z >> 8) >= A.thresh ? 4u : 0u) | ((ph.w >> 8) >= A.thresh ? 8u : 0u);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = 4 * g4 + e;
+        const float p = key0 + e <= q ? exp2f(sv[j] * A.scale_log2 - lse_q) : 0.0f;
+        float pd = p, dpd = dv[j];
+        if (A.thresh) {
+          const bool keep = (kb >> e) & 1u;
+          pd = keep ? p * A.dscale : 0.0f;
+          dpd = keep ? dpd * A.dscale : 0.0f;
+        }
+        pv[j] = pd;
+        gv[j] = p * (dpd - D_q);
+      }
+    }
+#pragma unroll
+    for (int h8 = 0; h8 < 2; ++h8) {
+      uint4 a, b;
+      a.x = pack2(pv[8 * h8], pv[8 * h8 + 1]);
+      a.y = pack2(pv[8 * h8 + 2], pv[8 * h8 + 3]);
+      a.z = pack2(pv[8 * h8 + 4], pv[8 * h8 + 5]);
+      a.w = pack2(pv[8 * h8 + 6], pv[8 * h8 + 7]);
+      b.x = pack2(gv[8 * h8], gv[8 * h8 + 1]);
+      b.y = pack2(gv[8 * h8 + 2], gv[8 * h8 + 3]);
+      b.z = pack2(gv[8 * h8 + 4], gv[8 * h8 + 5]);
+      b.w = pack2(gv[8 * h8 + 6], gv[8 * h8 + 7]);
+      const uint32_t off = hf * 16384 + sw_off(row, 2 * c + h8);
+      if (Pd) *reinterpret_cast<uint4*>(Pd + off) = a;
+      *reinterpret_cast<uint4*>(dS + off) = b;
+    }
+  }
+}
+
+// dK, dV of one 128-key tile: loop over the query tiles at or after it.
+__global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(AttnArgs A, const float* __restrict__ dO, int64_t ldo,
+                                                                 const float* __restrict__ lse, const float* __restrict__ D,
+                                                                 float* __restrict__ dqkv, int64_t ldg) {
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Ks = sm;
+  uint8_t* Vs = sm + 16384;
+  uint8_t* Qs = sm + 2 * 16384;
+  uint8_t* Os = sm + 3 * 16384;  // dO (bf16)
+  uint8_t* Ps = sm + 4 * 16384;  // Pd [128 q][128 k]
+  uint8_t* Gs = sm + 6 * 16384;  // dS [128 q][128 k]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 8 * 16384);  // [0] S, dP done; [1] dV, dK done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  const int kt = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int hf = w >> 2, row = (w & 3) * 32 + lane;
+  const int nq = A.seq / TCQ;
+  const int64_t base = (int64_t)s * A.seq;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  if (w == 0) tmem_alloc(tslot, 512);
+  load_sw_tile(A.qkv + (base + kt * TCQ) * A.ldq + A.d + h * HD, A.ldq, Ks);
+  load_sw_tile(A.qkv + (base + kt * TCQ) * A.ldq + 2 * A.d + h * HD, A.ldq, Vs);
+  cp_async_commit();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_off = (uint32_t)((w & 3) * 32) << 16;
+  const uint32_t tS = tmem + lane_off, tdP = tmem + 128 + lane_off;
+  constexpr uint32_t idSS = make_idesc_bf16(128, 128, false, false);  // S, dP: K-major Q / dO and K / V
+  constexpr uint32_t idT = make_idesc_bf16(128, 64, true, true);      // dV, dK: MN-major Pd^T / dS^T and dO / Q
+  const uint32_t pstep = A.thresh ? *A.step : 0u;
+  for (int qt = kt; qt < nq; ++qt) {
+    const int it = qt - kt;
+    if (it > 0) mbar_wait(&bar[1], (uint32_t)((it - 1) & 1));  // the previous dV / dK MMAs read Q, dO, Pd, dS
+    load_sw_tile(A.qkv + (base + qt * TCQ) * A.ldq + h * HD, A.ldq, Qs);
+    cp_async_commit();
+    load_sw_tile_f32(dO + (base + qt * TCQ) * ldo + h * HD, ldo, Os);
+    const int q = qt * TCQ + row;
+    const float lse_q = lse[(base + q) * A.nh + h], D_q = D[(base + q) * A.nh + h];
+    cp_async_wait<0>();
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        tc_mma_bf16(tmem, make_sdesc_sw128(smem_u32(Qs) + kk * 32, 16, 1024), make_sdesc_sw128(smem_u32(Ks) + kk * 32, 16, 1024),
+                    idSS, kk > 0);
+        tc_mma_bf16(tmem + 128, make_sdesc_sw128(smem_u32(Os) + kk * 32, 16, 1024),
+                    make_sdesc_sw128(smem_u32(Vs) + kk * 32, 16, 1024), idSS, kk > 0);
+      }
+      tc_commit(&bar[0]);
+    }
+    mbar_wait(&bar[0], (uint32_t)(it & 1));
+    tc_fence_after();
+    const uint64_t rowbase = (((uint64_t)(A.seq0 + s) * A.nh + h) * A.seq + q) * A.seq;
+    attn_bwd_tc_probs(A, tS, tdP, row, hf, q, kt, lse_q, D_q, rowbase, pstep, Ps, Gs);
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {  // K = the 128 queries, 16 per MMA
+        tc_mma_bf16(tmem + 256, make_sdesc_sw128(smem_u32(Ps) + kk * 2048, 16384, 1024),
+                    make_sdesc_sw128(smem_u32(Os) + kk * 2048, 8192, 1024), idT, (it | kk) ? 1u : 0u);
+        tc_mma_bf16(tmem + 320, make_sdesc_sw128(smem_u32(Gs) + kk * 2048, 16384, 1024),
+                    make_sdesc_sw128(smem_u32(Qs) + kk * 2048, 8192, 1024), idT, (it | kk) ? 1u : 0u);
+      }
+      tc_commit(&bar[1]);
+    }
+  }
+  mbar_wait(&bar[1], (uint32_t)((nq - 1 - kt) & 1));
+  tc_fence_after();
+  // TMEM lane = key row of the tile; this thread writes 32 of the 64 head columns of dK and dV
+  float dv[32], dk[32];
+  tmem_ld16(tmem + 256 + lane_off + hf * 32, dv);
+  tmem_ld16(tmem + 256 + lane_off + hf * 32 + 16, dv + 16);
+  tmem_ld16(tmem + 320 + lane_off + hf * 32, dk);
+  tmem_ld16(tmem + 320 + lane_off + hf * 32 + 16, dk + 16);
+  const int64_t grow = base + kt * TCQ + row;
+  float* kdst = dqkv + grow * ldg + A.d + h * HD + hf * 32;
+  float* vdst = dqkv + grow * ldg + 2 * A.d + h * HD + hf * 32;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    *reinterpret_cast<float4*>(kdst + 4 * c) =
+        make_float4(dk[4 * c] * A.scale, dk[4 * c + 1] * A.scale, dk[4 * c + 2] * A.scale, dk[4 * c + 3] * A.scale);
+    *reinterpret_cast<float4*>(vdst + 4 * c) = make_float4(dv[4 * c], dv[4 * c + 1], dv[4 * c + 2], dv[4 * c + 3]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 0) tmem_dealloc(tmem, 512);
+}
+
+// dQ of one 128-query tile: loop over the key tiles at or before it.
+__global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(AttnArgs A, const float* __restrict__ dO, int64_t ldo,
+                                                                const float* __restrict__ lse, const float* __restrict__ D,
+                                                                float* __restrict__ dqkv, int64_t ldg) {
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Qs = sm;
+  uint8_t* Os = sm + 16384;
+  uint8_t* Ks = sm + 2 * 16384;
+  uint8_t* Vs = sm + 3 * 16384;
+  uint8_t* Gs = sm + 4 * 16384;  // dS [128 q][128 k]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * 16384);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, s = blockIdx.z;  // heaviest first
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int hf = w >> 2, row = (w & 3) * 32 + lane;
+  const int64_t base = (int64_t)s * A.seq;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  if (w == 0) tmem_alloc(tslot, 512);
+  load_sw_tile(A.qkv + (base + qt * TCQ) * A.ldq + h * HD, A.ldq, Qs);
+  cp_async_commit();
+  load_sw_tile_f32(dO + (base + qt * TCQ) * ldo + h * HD, ldo, Os);
+  const int q = qt * TCQ + row;
+  const float lse_q = lse[(base + q) * A.nh + h], D_q = D[(base + q) * A.nh + h];
+  const uint64_t rowbase = (((uint64_t)(A.seq0 + s) * A.nh + h) * A.seq + q) * A.seq;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_off = (uint32_t)((w & 3) * 32) << 16;
+  const uint32_t tS = tmem + lane_off, tdP = tmem + 128 + lane_off;
+  constexpr uint32_t idSS = make_idesc_bf16(128, 128, false, false);
+  constexpr uint32_t idQ = make_idesc_bf16(128, 64, false, true);  // dQ: K-major dS, MN-major K
+  const uint32_t pstep = A.thresh ? *A.step : 0u;
+  for (int kt = 0; kt <= qt; ++kt) {
+    if (kt > 0) mbar_wait(&bar[1], (uint32_t)((kt - 1) & 1));  // the previous dQ MMAs read K and dS
+    load_sw_tile(A.qkv + (base + kt * TCQ) * A.ldq + A.d + h * HD, A.ldq, Ks);
+    load_sw_tile(A.qkv + (base + kt * TCQ) * A.ldq + 2 * A.d + h * HD, A.ldq, Vs);
+    cp_async_commit();
+    cp_async_wait<0>();
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        tc_mma_bf16(tmem, make_sdesc_sw128(smem_u32(Qs) + kk * 32, 16, 1024), make_sdesc_sw128(smem_u32(Ks) + kk * 32, 16, 1024),
+                    idSS, kk > 0);
+        tc_mma_bf16(tmem + 128, make_sdesc_sw128(smem_u32(Os) + kk * 32, 16, 1024),
+                    make_sdesc_sw128(smem_u32(Vs) + kk * 32, 16, 1024), idSS, kk > 0);
+      }
+      tc_commit(&bar[0]);
+    }
+    mbar_wait(&bar[0], (uint32_t)(kt & 1));
+    tc_fence_after();
+    attn_bwd_tc_probs(A, tS, tdP, row, hf, q, kt, lse_q, D_q, rowbase, pstep, nullptr, Gs);
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)  // K = the 128 keys, 16 per MMA
+        tc_mma_bf16(tmem + 256, make_sdesc_sw128(smem_u32(Gs) + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                    make_sdesc_sw128(smem_u32(Ks) + kk * 2048, 8192, 1024), idQ, (kt | kk) ? 1u : 0u);
+      tc_commit(&bar[1]);
+    }
+  }
+  mbar_wait(&bar[1], (uint32_t)(qt & 1));
+  tc_fence_after();
+  float dq[32];
+  tmem_ld16(tmem + 256 + lane_off + hf * 32, dq);
+  tmem_ld16(tmem + 256 + lane_off + hf * 32 + 16, dq + 16);
+  float* qdst = dqkv + (base + q) * ldg + h * HD + hf * 32;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<float4*>(qdst + 4 * c) =
+        make_float4(dq[4 * c] * A.scale, dq[4 * c + 1] * A.scale, dq[4 * c + 2] * A.scale, dq[4 * c + 3] * A.scale);
+  tc_fence_before();
+  __syncthreads();
+  if (w == 0) tmem_dealloc(tmem, 512);
+}
+
 // D[row][h] = sum_c dO[row][h*64 + c] * O[row][h*64 + c]  (= rowsum(P o dP), the softmax VJP term)
 __global__ void attn_bwd_prep_kernel(const float* __restrict__ dO, const __nv_bfloat16* __restrict__ O, int64_t ld,
                                      int rows, int nh, float* __restrict__ D) {
@@ -824,6 +1094,15 @@ int launch(const char* name, Kern k, dim3 grid, dim3 block, cudaStream_t st, Arg
 
 static int g_attn_tc = -1;  // -1: environment (TGP_ATTN_TC), else option "attn_tc"
 void attn_set_tc(int on) { g_attn_tc = on; }
+// tcgen05 attention (forward and backward, seq % 128 == 0) is the default; TGP_ATTN_TC=0 or option
+// attn_tc = 0 selects the mma.sync kernels (kept for comparison and for seq % 128 != 0)
+static bool attn_tc_on() {
+  static const bool tc_env = [] {
+    const char* e = getenv("TGP_ATTN_TC");
+    return !(e && e[0] == '0');
+  }();
+  return g_attn_tc < 0 ? tc_env : g_attn_tc != 0;
+}
 
 bool attn_shape_ok(int rows, int d, int nh, int seq) {
   return nh > 0 && d == nh * HD && seq % TILE == 0 && seq > 0 && rows % seq == 0;
@@ -838,12 +1117,7 @@ int attn_fwd(cudaStream_t st, const void* qkv, int rows, int d, int nh, int seq,
     return TGP_E_UNSUPPORTED;
   }
   AttnArgs A = make_args(qkv, rows, d, nh, seq, row_global0, thresh, dscale, seed, step, site);
-  static const bool tc_env = [] {  // opt-in: TGP_ATTN_TC=1 (measured: no faster than the split mma.sync path)
-    const char* e = getenv("TGP_ATTN_TC");
-    return e && e[0] == '1';
-  }();
-  const bool tc_on = g_attn_tc < 0 ? tc_env : g_attn_tc != 0;
-  if (tc_on && seq % TCQ == 0) {
+  if (attn_tc_on() && seq % TCQ == 0) {
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
@@ -901,6 +1175,29 @@ int attn_bwd(cudaStream_t st, const void* qkv, const void* ctx, const float* dO,
   const int warps = rows * nh;
   TGP_TRY(launch("attn_bwd_prep", attn_bwd_prep_kernel, dim3((warps + 3) / 4), dim3(128), st, dO,
                  (const __nv_bfloat16*)ctx, (int64_t)d, rows, nh, Dbuf));
+  if (attn_tc_on() && seq % TCQ == 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BTC_SMEM_KV);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(attn_bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BTC_SMEM_Q);
+      if (e != cudaSuccess) {
+        set_error("attn_bwd_tc smem attribute: %s", cudaGetErrorString(e));
+        return TGP_E_CUDA;
+      }
+      attr = true;
+    }
+    attn_bwd_dkv_tc_kernel<<<dim3(seq / TCQ, nh, rows / seq), 256, BTC_SMEM_KV, st>>>(A, dO, (int64_t)d, lse,
+                                                                                   (const float*)Dbuf, dqkv, 3 * (int64_t)d);
+    attn_bwd_dq_tc_kernel<<<dim3(seq / TCQ, nh, rows / seq), 256, BTC_SMEM_Q, st>>>(A, dO, (int64_t)d, lse,
+                                                                                 (const float*)Dbuf, dqkv, 3 * (int64_t)d);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_error("attn_bwd_tc launch: %s", cudaGetErrorString(e));
+      return TGP_E_CUDA;
+    }
+    return 0;
+  }
   TGP_TRY(launch("attn_bwd_dkv", attn_bwd_dkv_kernel, dim3(seq / TILE, nh, rows / seq), dim3(128), st, A, dO,
                  (int64_t)d, lse, (const float*)Dbuf, dqkv, 3 * (int64_t)d));
   return launch("attn_bwd_dq", attn_bwd_dq_kernel, dim3(seq / TILE, nh, rows / seq), dim3(128), st, A, dO, (int64_t)d,

@@ -39,14 +39,16 @@ def gpt_step(layers, params, x, t, *, m, n, ckpt, lr, balance=None, seed=0, opti
                grads=[P.get_grad(i) for i in range(P.n_params)], log=P.issue_log(), kernels=P.kernel_count())
     P.step(lr)
     rec["params"] = [P.get_param(i) for i in range(P.n_params)]
+    if options and "attn_tc" in options:
+        P.set_option("attn_tc", -1)  # the switch is process-wide: back to the default
     P.close()
     return rec
 
 
-def _run(layers, nseq, m, n, ckpt, balance=None, seed=11, lr=0.01):
+def _run(layers, nseq, m, n, ckpt, balance=None, seed=11, lr=0.01, options=None):
     x, t, params = make_case(layers, nseq, seed, "bf16")
     ref = oracle_step(layers, params, x, t, lr=lr, m=m, seed=seed, step=0)
-    gpu = gpt_step(layers, params, x, t, m=m, n=n, ckpt=ckpt, lr=lr, balance=balance, seed=seed)
+    gpu = gpt_step(layers, params, x, t, m=m, n=n, ckpt=ckpt, lr=lr, balance=balance, seed=seed, options=options)
     errs, bad = compare(gpu, ref, params, 2e-2, lr)
     assert not bad, f"errors above 2e-2: {bad}"
     return gpu, ref, errs
@@ -122,24 +124,34 @@ def test_c5_split_rows_attention():
     # seq 640 = 10 key tiles: query tiles 8 and 9 are split into two key ranges (partials merged in
     # fixed order); also checked against the checkpoint-free run bitwise (F' == F)
     layers = C.gpt2_stack(2, 128, 2, 640, 512, 0.1)
-    gpu, ref, errs = _run(layers, 2, 2, 2, "always", balance=[2, 2], seed=9)
+    gpu, ref, errs = _run(layers, 2, 2, 2, "always", balance=[2, 2], seed=9, options={"attn_tc": 0})
     x, t, params = make_case(layers, 2, 9, "bf16")
-    b = gpt_step(layers, params, x, t, m=2, n=2, ckpt="never", lr=0.01, balance=[2, 2], seed=9)
+    b = gpt_step(layers, params, x, t, m=2, n=2, ckpt="never", lr=0.01, balance=[2, 2], seed=9,
+                 options={"attn_tc": 0})
     assert b["loss"] == gpu["loss"] and np.array_equal(b["y"], gpu["y"])
 
 
-def test_c5_tcgen05_attention_forward():
-    # the tcgen05 attention forward (option attn_tc, seq % 128 == 0) against the oracle
-    layers = C.gpt2_stack(2, 128, 2, 256, 512, 0.1)
+@pytest.mark.parametrize("seq,nh", [(256, 2), (512, 3)])
+def test_c5_attention_tcgen05_vs_mma_sync(seq, nh):
+    # the tcgen05 attention (default: forward and the dK/dV + dQ backward on 128 x 128 tiles, S, dP
+    # and every transposed product on the tensor cores) and the mma.sync kernels (option attn_tc = 0)
+    # both against the oracle, and against each other (same arithmetic up to accumulation order)
+    layers = C.gpt2_stack(2, 64 * nh, nh, seq, 512, 0.1)
     x, t, params = make_case(layers, 2, 4, "bf16")
+    res = {}
     try:
-        gpu = gpt_step(layers, params, x, t, m=2, n=2, ckpt="always", lr=0.01, balance=[2, 2], seed=4,
-                       options={"attn_tc": 1})
+        for tc in (0, 1):
+            res[tc] = gpt_step(layers, params, x, t, m=2, n=2, ckpt="always", lr=0.01, balance=[2, 2], seed=4,
+                               options={"attn_tc": tc})
     finally:
         from paper_2004_09910_b200 import Pipeline  # reset the process-wide switch
         P = Pipeline(layers, chunks=2, devices=[0, 0], balance=[2, 2], max_batch=x.shape[0], dtype="bf16")
         P.set_option("attn_tc", -1)
         P.close()
     ref = oracle_step(layers, params, x, t, lr=0.01, m=2, seed=4, step=0)
-    errs, bad = compare(gpu, ref, params, 2e-2, 0.01)
-    assert not bad, bad
+    for tc in (0, 1):
+        errs, bad = compare(res[tc], ref, params, 2e-2, 0.01)
+        assert not bad, (tc, bad)
+    assert abs(res[0]["loss"] - res[1]["loss"]) <= 1e-4 * abs(res[0]["loss"])
+    for ga, gb in zip(res[0]["grads"], res[1]["grads"]):
+        assert np.max(np.abs(ga - gb)) <= 1e-2 * max(np.max(np.abs(ga)), 1e-12)
