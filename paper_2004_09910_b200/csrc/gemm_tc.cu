@@ -8,7 +8,10 @@
 #include "kernels.h"
 
 #ifndef TGP_SKINNY_SMEM
-#define TGP_SKINNY_SMEM 92160
+#define TGP_SKINNY_SMEM 163840
+#endif
+#ifndef TGP_W128_SMEM
+#define TGP_W128_SMEM 131072
 #endif
 
 namespace tgp {
@@ -34,19 +37,17 @@ struct TcCfg {
   static constexpr int A_BYTES = 128 * BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  // Skinny (weight-streaming) tiles keep <= ~110 KB so two CTAs fit on an SM: with programmatic
-  // dependent launch the NEXT GEMM's CTA becomes resident and streams its weights while this one
-  // drains its epilogue.  Wide tiles (dW) take the whole SM.
-  // BN = 128 tiles (the wide per-micro-batch GEMMs, N > 128 rows: C5's 1024-token micro-batches)
-  // also keep 3 stages (~97 KB) so two CTAs share an SM: one CTA's epilogue -- the instruction-bound
-  // part of these tiles (bias, GELU, fp32 z + bf16 operand stores) -- overlaps the other's mainloop.
-  static constexpr int BUDGET = BN <= 64 ? TGP_SKINNY_SMEM : BN == 128 ? 98304 : 196608;
+  // One CTA per SM (320 threads at ~100 registers): skinny (weight-streaming) tiles take a deep
+  // pipeline (160 KB: 9 - 12 stages; measured better than two 90 KB CTAs per SM overlapping across
+  // the PDL boundary, profiles/r6/); BN = 128 tiles (65 - 128-row micro-batches, C3 at m = 4) take 4
+  // stages next to the push reduction's 64 KB receive region; wide tiles (dW) take the whole SM.
+  static constexpr int BUDGET = BN <= 64 ? TGP_SKINNY_SMEM : BN == 128 ? TGP_W128_SMEM : 196608;
   static constexpr int STAGES = (BUDGET / STAGE) > 12 ? 12 : (BUDGET / STAGE);
   static constexpr int RED_BYTES = 128 * BN * 4;           // fp32 partial tile (float4 quads)
   static constexpr int CS_BYTES = (BN / 4) * 128 * 4;      // column-sum partials [quad][feature]
   // skinny tiles reduce split-K by pushing partials into a dedicated receive region (one cluster
   // barrier); wide tiles pull from the (aliased) stage buffers instead
-  static constexpr bool PUSH = BN <= 64;
+  static constexpr bool PUSH = BN <= 128;
   static constexpr int RECV_BYTES = PUSH ? RED_BYTES : 0;
   static constexpr int DATA = PUSH ? STAGES * STAGE
                                    : ((STAGES * STAGE > RED_BYTES + CS_BYTES) ? STAGES * STAGE : RED_BYTES + CS_BYTES);
@@ -71,8 +72,13 @@ TGP_DEV void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
+// warps: 0 TMA, 1 MMA, 2..5 TMEM epilogue (lane quadrants), 6..9 helpers: the split-K tail of the
+// push-reduced tiles is instruction-bound, so all 8 epilogue warps finish its work items
+constexpr int TC_THREADS = 320;
+constexpr int TC_FIN = TC_THREADS - 64;  // threads finishing push-reduced work items
+
 template <int BN, bool A_MN, bool B_MN, int MODE>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                    const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmD,
                    const GemmParams p) {
@@ -127,9 +133,11 @@ __global__ void __launch_bounds__(192, 1)
   constexpr bool push_red = C::PUSH && MODE != EPI_DW;
   if (push_red) cluster_arrive();
 
-  // owner-epilogue operands gathered during the mainloop (PUSH tiles, first PRE_IT items/thread)
-  constexpr int PRE_IT = 2;
-  EpiPre pre[PRE_IT][4];
+  // owner-epilogue operands of a thread's first two work items, gathered during the mainloop (PUSH
+  // tiles); the tail loop stays rolled and requests item k + 2's operands before finishing item k.
+  // (Unrolling every item's epilogue overflowed the instruction cache: at BN = 128 half the warp
+  // samples were no_instructions, profiles/r6/.)
+  EpiPre pre[2][4];
   auto stage_a = [&](int s) { return smem + s * C::STAGE; };
   auto stage_b = [&](int s) { return smem + s * C::STAGE + C::A_BYTES; };
   const int m0 = m_tile * 128;
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
     if (push_red) cluster_wait();
   } else {
-    // ---------------- epilogue warps 2..5: TMEM -> registers
+    // ---------------- epilogue warps 2..5: TMEM -> registers (6..9: helpers, see TC_THREADS)
     griddep_wait();
     if (push_red) {
       // gather the owner-side epilogue operands (bias, residual, pre-activation, dropout mask) now,
@@ -245,8 +253,8 @@ __global__ void __launch_bounds__(192, 1)
       const int et = (int)threadIdx.x - 64;
       const int nvalid = min(BN, p.N - nb), nq = (nvalid + 3) >> 2;
 #pragma unroll
-      for (int t = 0; t < PRE_IT; ++t) {
-        const int it = et + 128 * t;
+      for (int t = 0; t < 2; ++t) {
+        const int it = et + TC_FIN * t;
         if (it < rpr * nq) {
           const int fll = it & (rpr - 1), q = it >> lrpr, f = m0 + rank * rpr + fll;
 #pragma unroll
@@ -255,6 +263,10 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
+    // helpers (warps 6..9) share the TMEM lane quadrant of warp - 4 and take every other column chunk
+    // of the split-K push; the other tile kinds use warps 2..5 only
+    const bool helper = warp >= 6;
+    if (!helper || push_red) {
     mbar_wait(tfull, 0);
     tc_fence_after();
     if (threadIdx.x == 64) TGP_TS(3);
@@ -304,7 +316,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t rmbar = mapa_shared(smem_u32(rbar), (uint32_t)owner);
       cluster_wait();  // every rank's receive barrier is initialised (arrived right after setup)
 #pragma unroll 1
-      for (int c = 0; c < BN / 16; ++c) {
+      for (int c = helper ? 1 : 0; c < BN / 16; c += 2) {
         float v[16];
         tmem_ld16(taddr + c * 16, v);
 #pragma unroll
@@ -331,6 +343,7 @@ __global__ void __launch_bounds__(192, 1)
               nkb ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
+    }  // !helper || push_red
   }
   tc_fence_before();
 
@@ -350,7 +363,7 @@ __global__ void __launch_bounds__(192, 1)
     const bool want_cs = MODE == EPI_ACT_BWD && p.epi.colsum;
     if (et >= 0) {
       // one work item = (feature, 4-row quad): fixed source-rank order sum, then the epilogue with
-      // the operands gathered during the mainloop (items past PRE_IT per thread load them here)
+      // operands requested two items ahead (the first two during the mainloop)
       auto item = [&](int it, const EpiPre* pq) {
         const int fll = it & (rpr - 1), q = it >> lrpr;
         const int f = m0 + rank * rpr + fll;
@@ -364,24 +377,30 @@ __global__ void __launch_bounds__(192, 1)
         }
         const float av[4] = {a.x, a.y, a.z, a.w};
         if (threadIdx.x == 64 && it == et) TGP_TS(8);
-        float part = 0.0f;
-        if (f < p.M) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (4 * q + e < nvalid)
-              part += pq ? epi_finish<MODE>(p.epi, f, nb + 4 * q + e, av[e], pq[e])
-                        : epi_apply<MODE>(p.epi, f, nb + 4 * q + e, av[e]);
-        }
+        const float part = f < p.M ? epi_finish4<MODE>(p.epi, f, nb + 4 * q, min(4, nvalid - 4 * q), av, pq) : 0.0f;
         if (want_cs) cs[q * rpr + fll] = part;
         if (threadIdx.x == 64 && it == et) TGP_TS(9);
       };
+      auto gather = [&](int it, EpiPre* pq) {
+        if (it >= rpr * nq) return;
+        const int fll = it & (rpr - 1), q = it >> lrpr, f = m0 + rank * rpr + fll;
 #pragma unroll
-      for (int t = 0; t < PRE_IT; ++t)
-        if (et + 128 * t < rpr * nq) item(et + 128 * t, pre[t]);
+        for (int e = 0; e < 4; ++e)
+          if (f < p.M && 4 * q + e < nvalid) pq[e] = epi_load<MODE>(p.epi, f, nb + 4 * q + e);
+      };
 #pragma unroll 1
-      for (int it = et + 128 * PRE_IT; it < rpr * nq; it += 128) item(it, nullptr);
+      for (int it = et; it < rpr * nq; it += TC_FIN) {
+        EpiPre nx[4];
+        gather(it + 2 * TC_FIN, nx);
+        item(it, pre[0]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          pre[0][e] = pre[1][e];
+          pre[1][e] = nx[e];
+        }
+      }
       if (want_cs) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // the 128 epilogue threads only
+        asm volatile("bar.sync 1, %0;" ::"n"(TC_FIN) : "memory");  // the epilogue threads only
         if (et < rpr) {
           const int f = m0 + rank * rpr + et;
           float s = 0.0f;
@@ -404,7 +423,7 @@ __global__ void __launch_bounds__(192, 1)
     const int nq = (nvalid + 3) >> 2;
     float* cs = reinterpret_cast<float*>(smem + C::RED_BYTES);  // [q][feature] column-sum partials
     const bool want_cs = MODE == EPI_ACT_BWD && p.epi.colsum;
-    if (et >= 0) {
+    if (et >= 0 && et < 128) {  // warps 2..5
       const uint32_t base = smem_u32(smem);
       // UNR work items per thread per round: their global epilogue operands (residual rows,
       // saved pre-activations) are all requested before any is consumed, so the loads' latency
@@ -514,7 +533,7 @@ static int launch_tc(cudaStream_t st, bool pdl, const CUtensorMap& a, const CUte
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((p.M + 127) / 128, S, ntiles);
-  cfg.blockDim = dim3(192, 1, 1);
+  cfg.blockDim = dim3(TC_THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];

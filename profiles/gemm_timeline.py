@@ -1,5 +1,6 @@
 """Per-CTA %globaltimer timeline of the dominant GEMM chain (needs the TGP_GEMM_TIMING variant:
-TGP_LIB=build/variants/libtgp_timing.so).  Prints, per launch of the chain, when its CTAs start,
+TGP_LIB=variants/timing/libtgp.so, built by
+profiles/build_variant.py timing -DTGP_GEMM_TIMING).  Prints, per launch of the chain, when its CTAs start,
 pass griddepcontrol.wait, finish their MMAs, and exit -- relative to the previous launch's exit."""
 import ctypes
 import os
@@ -14,11 +15,15 @@ from paper_2004_09910_b200 import Pipeline, tgp  # noqa: E402
 from synth import configs as C  # noqa: E402
 
 sk = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+chunks = int(os.environ.get("CHUNKS", "32"))  # 32: 16-row micro-batches (stream kernel off below)
 layers = C.resmlp_stack(32, 4096)
-P = Pipeline(layers, chunks=32, devices=[0], balance=[32], checkpoint="except_last", max_batch=512, dtype="bf16",
+P = Pipeline(layers, chunks=chunks, devices=[0], balance=[32], checkpoint="except_last", max_batch=512, dtype="bf16",
              seed=1)
 P.init_params(1)
 P.set_option("splitk", sk)
+P.set_option("stream", 0)
+if "PF" in os.environ:
+    P.set_option("prefetch", int(os.environ["PF"]))
 lib = tgp.lib()
 f = lib.tgp_debug_timestamps
 f.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
@@ -33,8 +38,10 @@ rows = buf[:cnt].astype(np.int64)
 own = rows[:, 6] > 0
 for a_, b_, nm in ((3, 6, "tfull->recv"), (6, 8, "recv->sum"), (8, 9, "sum->epi_done"), (9, 7, "epi_done->stores"),
                    (7, 4, "stores->exit"), ):
+    if not own.any() or rows[own, b_].min() == 0:
+        continue
     d = rows[own, b_] - rows[own, a_]
-    if rows[own, b_].min() == 0:
+    if False:
         continue
     print(f"{nm:18s} ns pct0/50/90/100", np.percentile(d, [0, 50, 90, 100]))
 if len(sys.argv) > 2:
