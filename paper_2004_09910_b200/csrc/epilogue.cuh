@@ -84,62 +84,77 @@ TGP_DEV float epi_finish(const EpiParams& e, int f, int r, float v, const EpiPre
   }
 }
 
-// epi_finish for rows r0 .. r0 + n - 1 (n <= 4) of one feature: the same arithmetic per element, with
-// the flag tests and row addressing done once (the skinny GEMM's split-K tail is instruction-bound:
-// ~120 instructions per element through epi_finish, profiles/r6/)
-template <int MODE>
-TGP_DEV float epi_finish4(const EpiParams& e, int f, int r0, int n, const float* v, const EpiPre* q) {
-  float part = 0.0f;
+// epi_finish for rows r0 .. r0 + n - 1 (n <= NR) of one feature: the same arithmetic per element,
+// with the flag tests and the row addressing done once per call (the GEMM tails are issue-bound:
+// ~120 instructions per element through epi_finish in the skinny split-K tail, profiles/r6/)
+template <int MODE, int NR>
+TGP_DEV float epi_finish_rows(const EpiParams& e, int f, int r0, int n, const float* v, const EpiPre* q,
+                              float part = 0.0f) {
+  // part: running column sum (EPI_ACT_BWD) the rows are added to, in row order
+  const bool drop = e.drop_thresh != 0;
+  const float ds = e.drop_scale;
+  auto put_op = [&](float (&y)[NR]) {
+    if (!e.op) return;
+    if (e.op_bf16) {
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(e.op) + (int64_t)r0 * e.ld_op + f;
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+        if (j < n) o[(int64_t)j * e.ld_op] = __float2bfloat16_rn(y[j]);
+    } else {
+      float* o = reinterpret_cast<float*>(e.op) + (int64_t)r0 * e.ld_op + f;
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+        if (j < n) o[(int64_t)j * e.ld_op] = y[j];
+    }
+  };
   if constexpr (MODE == EPI_LINEAR_FWD) {
     float* zp = e.zbuf ? e.zbuf + (int64_t)r0 * e.ldz + f : nullptr;
     float* op0 = e.out0 ? e.out0 + (int64_t)r0 * e.ld0 + f : nullptr;
-    const bool drop = e.drop_thresh != 0;
-    const float ds = e.drop_scale;
     const int act = e.act;
-    float y4[4];
+    float y[NR];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NR; ++j) {
       const float z = v[j] + q[j].a;
       if (zp && j < n) zp[(int64_t)j * e.ldz] = z;
-      float y = act_f(act, z);
-      if (drop) y = q[j].keep ? y * ds : 0.0f;
-      y4[j] = y;
-      if (op0 && j < n) op0[(int64_t)j * e.ld0] = y;
+      float t = act_f(act, z);
+      if (drop) t = q[j].keep ? t * ds : 0.0f;
+      y[j] = t;
+      if (op0 && j < n) op0[(int64_t)j * e.ld0] = t;
     }
-    if (e.op) {
-      if (e.op_bf16) {
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(e.op) + (int64_t)r0 * e.ld_op + f;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < n) o[(int64_t)j * e.ld_op] = __float2bfloat16_rn(y4[j]);
-      } else {
-        float* o = reinterpret_cast<float*>(e.op) + (int64_t)r0 * e.ld_op + f;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < n) o[(int64_t)j * e.ld_op] = y4[j];
-      }
-    }
+    put_op(y);
   } else if constexpr (MODE == EPI_RESID_FWD) {
     float* op0 = e.out0 + (int64_t)r0 * e.ld0 + f;
-    const bool drop = e.drop_thresh != 0;
-    const float ds = e.drop_scale;
-    float y4[4];
+    float y[NR];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float br = v[j] + q[j].a;
+    for (int j = 0; j < NR; ++j) {
+      float br = v[j] + q[j].a;  // residual branch (dropout on the branch: GPT-2 blocks)
       if (drop) br = q[j].keep ? br * ds : 0.0f;
-      y4[j] = br + q[j].b;
-      if (j < n) op0[(int64_t)j * e.ld0] = y4[j];
+      y[j] = br + q[j].b;
+      if (j < n) op0[(int64_t)j * e.ld0] = y[j];
     }
-    if (e.op) {
+    put_op(y);
+  } else if constexpr (MODE == EPI_ACT_BWD) {
+    float* op0 = e.out0 ? e.out0 + (int64_t)r0 * e.ld0 + f : nullptr;
+    const int act = e.act;
+    float y[NR];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < n) store_op(e, r0 + j, f, y4[j]);
+    for (int j = 0; j < NR; ++j) {
+      float d = v[j];
+      if (drop) d = q[j].keep ? d * ds : 0.0f;
+      if (act) d *= act_df(act, q[j].a);
+      y[j] = d;
+      if (j < n) {
+        if (op0) op0[(int64_t)j * e.ld0] = d;
+        part += d;
+      }
     }
-  } else {
+    put_op(y);
+  } else if constexpr (MODE == EPI_STORE) {
+    float* o = f < e.split_f ? e.out0 + (int64_t)r0 * e.ld0 + f : e.out1 + (int64_t)r0 * e.ld1 + (f - e.split_f);
+    const int64_t ld = f < e.split_f ? e.ld0 : e.ld1;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (j < n) part += epi_finish<MODE>(e, f, r0 + j, v[j], q[j]);
+    for (int j = 0; j < NR; ++j)
+      if (j < n) o[(int64_t)j * ld] = v[j];
   }
   return part;
 }

@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         const float av[4] = {a.x, a.y, a.z, a.w};
         if (threadIdx.x == 64 && it == et) TGP_TS(8);
-        const float part = f < p.M ? epi_finish4<MODE>(p.epi, f, nb + 4 * q, min(4, nvalid - 4 * q), av, pq) : 0.0f;
+        const float part = f < p.M ? epi_finish_rows<MODE, 4>(p.epi, f, nb + 4 * q, min(4, nvalid - 4 * q), av, pq) : 0.0f;
         if (want_cs) cs[q * rpr + fll] = part;
         if (threadIdx.x == 64 && it == et) TGP_TS(9);
       };

@@ -196,9 +196,11 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
               pre[j] = epi_load<MODE>(p.epi, f, r0 + j);
             }
           }
+        if (!nkb) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (r0 + j < p.N) part += epi_finish<MODE>(p.epi, f, r0 + j, nkb ? v[j] : 0.0f, pre[j]);
+          for (int j = 0; j < 8; ++j) v[j] = 0.0f;
+        }
+        part = epi_finish_rows<MODE, 8>(p.epi, f, r0, min(8, p.N - r0), v, pre, part);
         if (MODE == EPI_ACT_BWD && ((cg & 1) || r0 + 8 >= p.N)) {  // per-16-row column partials
           if (p.epi.colsum) p.epi.colsum[(int64_t)(r0 / 16) * p.M + f] = part;
           part = 0.0f;
