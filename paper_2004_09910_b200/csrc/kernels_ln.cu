@@ -306,6 +306,12 @@ int ln_bwd_cl(cudaStream_t st, bool pdl, const float* dh, const float* x, const 
     set_error("ln_bwd_cl: no cluster shape for d=%d", d);
     return -5;
   }
+  // from 64 rows: clusters of 16 (non-portable size), twice the CTAs of the 8-wide split (C3 m = 4: B
+  // task 1376 -> 1244 us, profiles/r6/)
+  if (rowblocks >= 4 && CL == 8 && NQ >= 64) {
+    CL = 16;
+    NQ /= 2;
+  }
 #define L_(N)                                                                                                   \
   if (NQ == N)                                                                                                  \
     return launch_cluster("ln_bwd_cl", ln_bwd_cl_kernel<N>, CL, rowblocks, st, pdl, dh, x, mean, rstd, gamma, dy, \
