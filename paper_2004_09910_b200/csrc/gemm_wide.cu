@@ -25,7 +25,10 @@ namespace tgp {
 namespace {
 constexpr int WG_BM = 128, WG_BN = 128, WG_BK = 64;
 constexpr int WG_STAGE = (WG_BM + WG_BN) * WG_BK * 2;  // 32 KB
-constexpr int WG_STAGES = 6;
+#ifndef TGP_WG_STAGES
+#define TGP_WG_STAGES 6
+#endif
+constexpr int WG_STAGES = TGP_WG_STAGES;
 constexpr int WG_OFF_BAR = WG_STAGES * WG_STAGE;
 constexpr int WG_SMEM = WG_OFF_BAR + 256 + 1024;
 // The epilogue, not the MMA, bounds these tiles (~40 instructions per element vs 5.5 us of tensor

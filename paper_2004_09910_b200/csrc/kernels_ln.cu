@@ -308,9 +308,26 @@ int ln_bwd_cl(cudaStream_t st, bool pdl, const float* dh, const float* x, const 
   }
   // from 64 rows: clusters of 16 (non-portable size), twice the CTAs of the 8-wide split (C3 m = 4: B
   // task 1376 -> 1244 us, profiles/r6/)
-  if (rowblocks >= 4 && CL == 8 && NQ >= 64) {
+  static int cl16 = -1;  // can this device co-schedule a cluster of 16 of these CTAs?
+  if (cl16 < 0) {
+    cudaFuncSetAttribute(ln_bwd_cl_kernel<64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16, 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 16;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cl16 = (cudaOccupancyMaxActiveClusters(&n, ln_bwd_cl_kernel<64>, &cfg) == cudaSuccess && n > 0) ? 1 : 0;
+    cudaGetLastError();
+  }
+  if (cl16 && rowblocks >= 4 && CL == 8 && NQ == 128) {
     CL = 16;
-    NQ /= 2;
+    NQ = 64;
   }
 #define L_(N)                                                                                                   \
   if (NQ == N)                                                                                                  \
