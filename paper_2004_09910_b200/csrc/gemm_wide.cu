@@ -26,7 +26,7 @@ namespace {
 constexpr int WG_BM = 128, WG_BN = 128, WG_BK = 64;
 constexpr int WG_STAGE = (WG_BM + WG_BN) * WG_BK * 2;  // 32 KB
 #ifndef TGP_WG_STAGES
-#define TGP_WG_STAGES 6
+#define TGP_WG_STAGES 7
 #endif
 constexpr int WG_STAGES = TGP_WG_STAGES;
 constexpr int WG_OFF_BAR = WG_STAGES * WG_STAGE;
