@@ -333,7 +333,8 @@ def run_tgp(args):
     gemm_ms, gemm_bytes, gemm_n = P.bench_dominant_gemm(rank, BATCH, reps=10 if stream else 3)
     mrows = BATCH // args.chunks
     kname = (f"task_stream_kernel F task ({BLOCKS // n} blocks x 2 weight-streaming GEMMs, M={mrows} rows, d=H={WIDTH})"
-             if stream else f"gemm_tc_kernel forward W1 GEMM (M={mrows} rows, K=N={WIDTH})")
+             if stream else f"{'gemm_wide_kernel' if mrows >= 256 else 'gemm_tc_kernel'} forward W1 GEMM "
+             f"(M={mrows} rows, K=N={WIDTH})")
     peaks = _peaks()
     if peaks and "hbm_gbs" in peaks:
         peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
