@@ -15,7 +15,8 @@
  *  - Partitions are numbered j = 0..n_parts-1 in this ABI (the paper's j = 1..n).
  *  - Matrices are row-major [rows][features], fp32, device memory unless stated "host".
  *  - Calls are blocking: they return after all device work THIS PROCESS issued for the call has
- *    completed (host timing around a call is valid; no hidden asynchronous state).
+ *    completed (host timing around a call is valid; no hidden asynchronous state) -- except the
+ *    *_async variants below, which are stream-ordered and return without a host wait.
  *  - A context is not thread-safe: one host thread drives it.
  *  - No CPU fallback: a process without a usable sm_100 GPU gets TGP_E_CUDA / TGP_E_UNSUPPORTED
  *    from tgp_create.  Pure host entry points (tgp_balance, tgp_split, tgp_schedule) need no GPU.
@@ -214,6 +215,31 @@ tgp_status tgp_step(tgp_ctx* ctx, float lr);
  * them).  Every other parameter, and fp32 mode, takes the unfused path.  Arguments as tgp_backward.
  * TGP_E_STATE if gradients of an earlier tgp_backward are still pending (call tgp_step first). */
 tgp_status tgp_backward_step(tgp_ctx* ctx, const float* dy, float* dx, float lr);
+
+/* ------------------------------------------------------------------ asynchronous, stream-ordered calls
+ * (PAPER.md P:133 and Alg. 1: the host only issues tasks, the devices wait on
+ * one another).  Each call below issues exactly the device work of its blocking twin (same arguments,
+ * same results bit for bit) and returns as soon as it is issued:
+ *  - ordering: the work starts after everything queued on `stream` before the call (so inputs may
+ *    still be in production on `stream`), and `stream` waits for the call's work on every local
+ *    partition (so work queued on `stream` afterwards sees the results).  `stream` is a cudaStream_t
+ *    (NULL = the legacy default stream of the current device), cast to void* so this header needs no
+ *    CUDA include; it may live on any device;
+ *  - buffers: x, y, dy, dx, target, loss_dev must stay allocated and unmodified (outputs: unread)
+ *    until `stream` reaches the call's completion;
+ *  - errors: argument and state errors are reported at issue time exactly as by the blocking twin;
+ *    device-side failures and a lost cross-partition message surface at the next tgp_sync (or the next
+ *    blocking call) -- TGP_E_CUDA / TGP_E_TIMEOUT with the watchdog semantics above;
+ *  - tracing (tgp_set_trace): timeline records of async calls become readable after tgp_sync. */
+tgp_status tgp_forward_async(tgp_ctx* ctx, const float* x, int32_t B, float* y, void* stream);
+/* loss_dev: DEVICE pointer to one double (the MSE loss), on the last partition's device, may be NULL */
+tgp_status tgp_mse_loss_grad_async(tgp_ctx* ctx, const float* y, const float* target, int32_t B, float* dy,
+                                   double* loss_dev, void* stream);
+tgp_status tgp_backward_async(tgp_ctx* ctx, const float* dy, float* dx, void* stream);
+tgp_status tgp_backward_step_async(tgp_ctx* ctx, const float* dy, float* dx, float lr, void* stream);
+tgp_status tgp_step_async(tgp_ctx* ctx, float lr, void* stream);
+/* Bounded host wait for every call issued so far on this context (TGP_E_TIMEOUT past "watchdog_ms"). */
+tgp_status tgp_sync(tgp_ctx* ctx);
 
 /* ------------------------------------------------------------------ parameters / introspection */
 

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -988,6 +989,11 @@ static int write_flag(cudaStream_t st, uint32_t* flag, uint32_t v) {
   return 0;
 }
 
+// 4-byte value into device memory, ordered on the stream (no host staging buffer: asynchronous calls
+// may return before it executes)
+static int put_u32(cudaStream_t st, void* dst, uint32_t v) { return write_flag(st, (uint32_t*)dst, v); }
+
+
 static void trace_begin(tgp_ctx* c, Stage& s, cudaStream_t st, int stream_id, int kind, int i, cudaEvent_t* a) {
   if (!c->trace) return;
   cudaEventCreate(a);
@@ -1258,7 +1264,9 @@ static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>
       if (c->fuse_sgd && s.grads_fresh && c->bf16) {
         // W_j + SGD (tgp_backward_step): the learning rate is a device scalar, so the graph replays
         TGP_TRY(ensure_ws(c, s, B));
-        TGP_CUDA_TRY(cudaMemcpyAsync(s.dlr, &c->lr_host, 4, cudaMemcpyHostToDevice, s.comp));
+        uint32_t lr_bits;
+        std::memcpy(&lr_bits, &c->lr_host, 4);
+        TGP_TRY(put_u32(s.comp, s.dlr, lr_bits));
         TGP_TRY(run_task(c, s, s.gWs, B, [&] { return exec_wgrad(c, s, B, true); }));
         s.grads_fresh = true;  // consumed by the fused step
       } else if (s.grads_fresh) {
@@ -1344,6 +1352,71 @@ static int sync_with_watchdog(tgp_ctx* c) {
   return 0;
 }
 
+// Timeline records of the finished calls (needs their events complete: after a host wait).
+static void drain_trace(tgp_ctx* c) {
+  for (auto& t : c->trace_recs) {
+    Stage* s = c->local[t.part];
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, s->ev_epoch, t.a);
+    cudaEventElapsedTime(&b, s->ev_epoch, t.b);
+    int64_t rec[6] = {t.part, t.stream, t.kind, t.i, (int64_t)(a * 1e6), (int64_t)(b * 1e6)};
+    c->timeline.insert(c->timeline.end(), rec, rec + 6);
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  c->trace_recs.clear();
+}
+
+// Asynchronous stream-ordered calls (tgp_*_async).  enter: every local partition's
+// compute stream waits for the work the caller queued on `st` before the call (its inputs' producers);
+// leave: each partition joins its other lanes (comp2, copy streams) into comp, and `st` waits for every
+// partition, so whatever the caller queues next on `st` sees the call's results.  No host wait.
+static int async_enter(tgp_ctx* c, cudaStream_t st) {
+  int dev = -1;
+  if (cudaStreamGetDevice(st, &dev) != cudaSuccess) {
+    cudaGetLastError();
+    TGP_CUDA_TRY(cudaGetDevice(&dev));
+  }
+  if (!c->ev_user || c->ev_user_dev != dev) {
+    TGP_CUDA_TRY(cudaSetDevice(dev));
+    if (c->ev_user) cudaEventDestroy(c->ev_user);
+    c->ev_user = nullptr;
+    TGP_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming));
+    c->ev_user_dev = dev;
+  }
+  TGP_CUDA_TRY(cudaSetDevice(dev));
+  TGP_CUDA_TRY(cudaEventRecord(c->ev_user, st));
+  for (Stage* s : c->local)
+    if (s) {
+      TGP_CUDA_TRY(cudaSetDevice(s->dev));
+      TGP_CUDA_TRY(cudaStreamWaitEvent(s->comp, c->ev_user, 0));
+    }
+  c->async_call = true;
+  c->ustream = st;
+  return 0;
+}
+
+static int async_leave(tgp_ctx* c) {
+  cudaStream_t st = c->ustream;
+  c->async_call = false;
+  c->ustream = nullptr;
+  for (Stage* s : c->local) {
+    if (!s) continue;
+    TGP_CUDA_TRY(cudaSetDevice(s->dev));
+    const cudaStream_t lanes[3] = {s->comp2, s->cact, s->cskip};
+    for (int k = 0; k < 3; ++k)
+      if (lanes[k]) {
+        TGP_CUDA_TRY(cudaEventRecord(s->ev_join[k], lanes[k]));
+        TGP_CUDA_TRY(cudaStreamWaitEvent(s->comp, s->ev_join[k], 0));
+      }
+    TGP_CUDA_TRY(cudaEventRecord(s->ev_done, s->comp));
+  }
+  TGP_CUDA_TRY(cudaSetDevice(c->ev_user_dev));
+  for (Stage* s : c->local)
+    if (s) TGP_CUDA_TRY(cudaStreamWaitEvent(st, s->ev_done, 0));
+  return 0;
+}
+
 static int finish_call(tgp_ctx* c) {
   // tell every partition that writes into a local partition that this call is done on it
   for (int j = 0; j < c->n; ++j) {
@@ -1354,20 +1427,9 @@ static int finish_call(tgp_ctx* c) {
       c->kernels++;
     }
   }
+  if (c->async_call) return 0;  // the caller's stream is joined by async_leave; tgp_sync waits
   TGP_TRY(sync_with_watchdog(c));
-  if (c->trace) {
-    for (auto& t : c->trace_recs) {
-      Stage* s = c->local[t.part];
-      float a = 0, b = 0;
-      cudaEventElapsedTime(&a, s->ev_epoch, t.a);
-      cudaEventElapsedTime(&b, s->ev_epoch, t.b);
-      int64_t rec[6] = {t.part, t.stream, t.kind, t.i, (int64_t)(a * 1e6), (int64_t)(b * 1e6)};
-      c->timeline.insert(c->timeline.end(), rec, rec + 6);
-      cudaEventDestroy(t.a);
-      cudaEventDestroy(t.b);
-    }
-    c->trace_recs.clear();
-  }
+  if (c->trace) drain_trace(c);
   return 0;
 }
 
@@ -1378,7 +1440,7 @@ static int begin_call(tgp_ctx* c) {
   for (Stage* s : c->local)
     if (s) {  // the fused-send flags carry the call's sequence number (read on the device)
       TGP_CUDA_TRY(cudaSetDevice(s->dev));
-      TGP_CUDA_TRY(cudaMemcpyAsync(s->dseq, &c->seq, 4, cudaMemcpyHostToDevice, s->comp));
+      TGP_TRY(put_u32(s->comp, s->dseq, c->seq));
     }
   for (int j = 0; j < c->n; ++j) {
     Stage* sp = c->local[j];
@@ -1388,6 +1450,7 @@ static int begin_call(tgp_ctx* c) {
     // copy streams must not run ahead of the call's start (events of the previous call)
     TGP_CUDA_TRY(cudaStreamWaitEvent(sp->cact, sp->ev_start, 0));
     TGP_CUDA_TRY(cudaStreamWaitEvent(sp->cskip, sp->ev_start, 0));
+    if (sp->comp2) TGP_CUDA_TRY(cudaStreamWaitEvent(sp->comp2, sp->ev_start, 0));
   }
   return 0;
 }

@@ -136,6 +136,9 @@ struct Stage {
   unsigned* st_cnt2 = nullptr;
   float* st_stats2 = nullptr;
   cudaEvent_t ev_pair = nullptr;      // recorded on comp before a paired B: lane 1 waits for it
+  cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};  // async calls: comp2 / cact / cskip joined into comp
+  cudaEvent_t ev_done = nullptr;
+  int bn_rows_B = -1;                 // mini-batch size bn_rows was last written for      // async calls: the partition's share of the call is done (on comp)
   std::vector<cudaEvent_t> rdone;     // per micro-batch: its hoisted F' finished (recorded on comp2)
   std::vector<char> hoisted;          // per micro-batch: F' already issued on lane 1 in this call
   std::vector<TaskGraph> gR2, gB2;    // paired-task graphs (half grid)
@@ -219,6 +222,12 @@ struct tgp_ctx {
   std::vector<int64_t> timeline;
   std::vector<std::pair<int, int>> route_parts_1b;
   bool connected = true;
+  // asynchronous stream-ordered calls (tgp_*_async): the caller's stream while such a
+  // call is being issued, and the event its work is ordered after (created on the stream's device)
+  bool async_call = false;
+  cudaStream_t ustream = nullptr;
+  cudaEvent_t ev_user = nullptr;
+  int ev_user_dev = -1;
   int n_params = 0;
   std::vector<int> param_layer, param_local;
 };

@@ -105,6 +105,20 @@ TGP_DEV unsigned ld_relaxed_u32(const unsigned* p) {
   return v;
 }
 TGP_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Acquire side of a counter that a relaxed poll has seen reach its target: one ld.acquire re-read of
+// the counter (LDG.STRONG + L1 invalidate) instead of a full fence (MEMBAR.ALL.GPU, which also waits
+// for the warp's outstanding memory operations).  The counter only grows within a task and every
+// increment is a release RMW, so the acquire synchronises with all of them.
+TGP_DEV void acquire_counter(const unsigned* p) {
+#ifndef TGP_ST_FENCE_ACQ
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  (void)v;
+#else
+  (void)p;
+  fence_acq_rel_gpu();
+#endif
+}
 TGP_DEV void st_release_cta_u32(uint32_t saddr, uint32_t v) {
   asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
@@ -459,7 +473,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
         const unsigned need = (unsigned)(phase_of(t, p).K / 128);
         const unsigned* dep = cnt(1 + 3 * (p >> 1) + (p & 1), rank);
         while (ld_relaxed_u32(dep) < need) __nanosleep(t.sleep_ns);
-        fence_acq_rel_gpu();
+        acquire_counter(dep);
         st_release_cta_u32(released, (uint32_t)(p + 1));
       }
     }
@@ -502,7 +516,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
     auto wait_cnt = [&](int id, int q, unsigned need) {
       if (et == 0) {
         while (ld_relaxed_u32(cnt(id, q)) < need) __nanosleep(t.sleep_ns);
-        fence_acq_rel_gpu();
+        acquire_counter(cnt(id, q));
         dbg_stamp(t, cur_p, 8);
       }
       epi_bar();

@@ -63,6 +63,12 @@ _SIGS = {
     "tgp_backward": [_P, _P, _P],
     "tgp_step": [_P, ctypes.c_float],
     "tgp_backward_step": [_P, _P, _P, ctypes.c_float],
+    "tgp_forward_async": [_P, _P, _I32, _P, _P],
+    "tgp_mse_loss_grad_async": [_P, _P, _P, _I32, _P, _P, _P],
+    "tgp_backward_async": [_P, _P, _P, _P],
+    "tgp_backward_step_async": [_P, _P, _P, ctypes.c_float, _P],
+    "tgp_step_async": [_P, ctypes.c_float, _P],
+    "tgp_sync": [_P],
     "tgp_num_params": [_P, ctypes.POINTER(_I32)],
     "tgp_param_info": [_P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I64)],
     "tgp_set_param": [_P, _I32, _P],
@@ -270,6 +276,41 @@ class Pipeline:
         """tgp_backward + tgp_step(lr) with SGD fused into W_j (fused weight gradients not stored)."""
         _ready(dy, dx)
         _check(lib().tgp_backward_step(self.h, _ptr(dy), _ptr(dx), ctypes.c_float(lr)), "tgp_backward_step")
+
+    # ---- asynchronous, stream-ordered variants (include/tgp.h): no host wait, no _ready(); the
+    # work is ordered after what is queued on `stream` (default: torch's current stream of the
+    # tensor's device) and `stream` waits for it
+    @staticmethod
+    def _stream(stream, t):
+        if stream is not None:
+            return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.current_stream(t.device if t is not None else None).cuda_stream)
+
+    def forward_async(self, x, B, y, stream=None):
+        _check(lib().tgp_forward_async(self.h, _ptr(x), B, _ptr(y), self._stream(stream, x if x is not None else y)),
+               "tgp_forward_async")
+
+    def mse_loss_grad_async(self, y, t, B, dy, loss_dev=None, stream=None):
+        """loss_dev: a float64 CUDA tensor of >= 1 element on y's device (or None)."""
+        _check(lib().tgp_mse_loss_grad_async(self.h, _ptr(y), _ptr(t), B, _ptr(dy), _ptr(loss_dev),
+                                             self._stream(stream, y)), "tgp_mse_loss_grad_async")
+
+    def backward_async(self, dy, dx=None, stream=None):
+        _check(lib().tgp_backward_async(self.h, _ptr(dy), _ptr(dx), self._stream(stream, dy if dy is not None else dx)),
+               "tgp_backward_async")
+
+    def backward_step_async(self, dy, lr, dx=None, stream=None):
+        _check(lib().tgp_backward_step_async(self.h, _ptr(dy), _ptr(dx), ctypes.c_float(lr),
+                                             self._stream(stream, dy if dy is not None else dx)),
+               "tgp_backward_step_async")
+
+    def step_async(self, lr, stream=None):
+        _check(lib().tgp_step_async(self.h, ctypes.c_float(lr), self._stream(stream, None)), "tgp_step_async")
+
+    def sync(self):
+        _check(lib().tgp_sync(self.h), "tgp_sync")
 
     # ---- parameters
     def param_info(self, idx):
