@@ -4,6 +4,7 @@
 // checkpointing), P:198-203 (copy streams), P:212 (checkpoint slot shared with the receive
 // buffer), P:242-245 (portals: one direct copy per skip tensor), P:70 (g = sum_i g_i), P:307 (SGD).
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -1056,7 +1057,39 @@ static std::vector<int> writers_of(const tgp_ctx* c, int j) {
 // Issue one schedule record whose actor is local.  Copies ride on the producer's copy streams and
 // end with a flag release on the consumer; computes wait on their receive flags on the compute
 // stream (the consumer never blocks the producer).
+// NVTX ranges (host issue side; SURVEY 5 tracing, Fig. 7): one range per tgp_* call and
+// per issued task, named after the schedule record ("F i=3 j=2", "COPY_B i=1 2->1", "W j=1"), so a
+// profiler timeline lines the host issue order up against the device work.  Header-only NVTX 3: a
+// no-op pointer check when no tool is attached.  Option "nvtx" (default 1).
+struct NvtxRange {
+  bool on;
+  NvtxRange(const tgp_ctx* c, const char* name) : on(c->nvtx) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
+static const char* kind_name(int k) {
+  static const char* names[] = {"F", "F'", "B", "COPY_F", "COPY_B", "SKIP_F", "SKIP_B", "W"};
+  return (k >= 0 && k < 8) ? names[k] : "?";
+}
+
+static int issue_task(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>>& first_push);
 static int issue(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>>& first_push) {
+  if (!c->nvtx) return issue_task(c, rc, B, first_push);
+  char name[64];
+  if (rc.kind == K_W)
+    snprintf(name, sizeof(name), "W j=%d", rc.j);
+  else if (rc.kind >= K_COPY_F)
+    snprintf(name, sizeof(name), "%s i=%d %d->%d r=%d", kind_name(rc.kind), rc.i, rc.src, rc.dst, rc.route);
+  else
+    snprintf(name, sizeof(name), "%s i=%d j=%d", kind_name(rc.kind), rc.i, rc.j);
+  NvtxRange r(c, name);
+  return issue_task(c, rc, B, first_push);
+}
+
+static int issue_task(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<char>>& first_push) {
   const int i = rc.i;
   int r0 = 0, M = 0;
   if (i > 0) micro_rows(c, B, i, &r0, &M);

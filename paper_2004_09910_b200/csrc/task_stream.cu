@@ -220,6 +220,8 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
   // phases < *released have their activation dependency met (written by the poller warp with
   // st.release.cta after its gpu-scope acquire; read by the producer with ld.acquire.cta)
   const uint32_t released = smem_u32(smem + OFF_BAR + 6144);
+  // loaded phases whose MMAs have started (MMA issuer, st.release.cta; read by the copy warps)
+  const uint32_t mstart = smem_u32(smem + OFF_BAR + 6176);
   auto recv_bytes = [&](int u) { return (uint32_t)(SK * 32 * ncol(u / NV) * 4); };
   auto cnt = [&](int id, int q) { return t.cnt + ((size_t)id * 5 + q) * CNT_STRIDE; };
 
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
       for (int g = 0; g < 2; ++g)
         for (int k = ng[g]; k < 128; ++k) grp_list[g * 128 + k] = (uint16_t)NU;
     st_release_cta_u32(released, 0u);
+    st_release_cta_u32(mstart, 0u);
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 4);
@@ -359,7 +362,10 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
         const uint32_t idesc = ncol(p) == 32 ? idesc32 : idesc16;
         const int buf = ng[grp] & 1, uu = ng[grp] >> 1;
         mbar_wait(&tempty[grp * 2 + buf], (uint32_t)((uu & 1) ^ 1));
-        if (first) mbar_wait(bfull, (uint32_t)(nload & 1));
+        if (first) {
+          mbar_wait(bfull, (uint32_t)(nload & 1));
+          if constexpr (NV == 1) st_release_cta_u32(mstart, (uint32_t)(nload + 1));
+        }
         tc_fence_after();
         const uint32_t dacc = tmem + (uint32_t)(grp * 64 + buf * 32);
         for (int kb = 0; kb < nkb; ++kb, ++g) {
@@ -405,10 +411,15 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
     const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)ACC;
     const uint32_t ring0 = smem_u32(ring);
     int g = 0;
+    int pord = -1, lastp = -1, dph = 0;  // loaded-phase ordinal of the tile, MMA-complete phases
     for (int k = 0; k < NU; ++k) {
       const int u = nth_active(k);
       if (u >= NU) break;
       const int p = u / NV;
+      if (p != lastp) {
+        ++pord;
+        lastp = p;
+      }
       const int nkb = phase_of(t, p).K / (SK * 64);
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int s = g % NST, r = g / NST;
@@ -447,6 +458,17 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // the ring stage is free (the tile is in registers)
         mbar_wait(&aempty[slot >> 1], (uint32_t)((rs & 1) ^ 1));
+        if constexpr (NV == 1) {
+          // full grid: a tile of a LATER phase waits while the current phase's MMAs run (its
+          // tcgen05.st would share TMEM bandwidth with their A-operand reads; F task 512 -> 481 us);
+          // tiles of the running phase go at once.  Not on the half grid of a paired task, whose 32
+          // tiles per phase need every copy slot (measured: paired F' + B 976 -> 1196 us).
+          while (true) {
+            const int st = (int)ld_acquire_cta_u32(mstart);
+            while (dph < st && mbar_test_wait(smem_u32(bempty), (uint32_t)(dph & 1))) ++dph;
+            if (!(st > dph && pord >= st)) break;
+          }
+        }
         tc_fence_after();
         tmem_st32(trow + (uint32_t)(slot * 32), v);
         tmem_st_wait();
