@@ -144,11 +144,6 @@ TGP_DEV uint4 lds_u128(uint32_t a) {
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
   return v;
 }
-TGP_DEV uint32_t lds_u16(uint32_t a) {
-  unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
-  return (uint32_t)v;
-}
 // 32 lanes x 32 bit, 32 consecutive columns per thread (thread = lane of its warp's quadrant)
 TGP_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -161,6 +156,20 @@ TGP_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 TGP_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 16 lanes x 256 bit: thread t writes lane t/4 (r0, r1) and lane t/4 + 8 (r2, r3), columns 2(t%4), +1
+TGP_DEV void tmem_st_16x256b(uint32_t taddr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r0), "r"(r1), "r"(r2),
+               "r"(r3)
+               : "memory");
+}
+// four 8x8 b16 matrices, transposed: thread t gets {M[2(t%4)][t/4], M[2(t%4)+1][t/4]} of matrix i in
+// register i; threads 8i..8i+7 give the row addresses of matrix i
+TGP_DEV void ldsm_x4_trans(uint32_t a, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a)
+               : "memory");
+}
 
 template <typename T>
 TGP_DEV T wsum32(T v) {
@@ -439,15 +448,23 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
           }
         } else {
           // MN-major tile: two [64 k][64 f] halves of 8 KB, element (k, f) of half f / 64 in 128-byte
-          // row k, 16-byte chunk ((f % 64) / 8) ^ (k & 7), position f % 8 (the transpose of A)
-          const uint32_t hb = base + (uint32_t)((f >> 6) * 8192 + (f & 7) * 2);
-          const int j = (f & 63) >> 3;
+          // row k, 16-byte chunk ((f % 64) / 8) ^ (k & 7), position f % 8 (the transpose of A).
+          // Transposed 8x8 loads straight into the 16x256b TMEM-store fragment: chunk (h2, cc) =
+          // lanes 32q + 16 h2 + [0, 16) (feature groups jj = 4q + 2 h2 + {0, 1}) x k-pair columns
+          // 8 cc + [0, 8).  Matrix i = (jj offset i / 2, k rows 16 cc + {0,1,4,5,8,9,12,13} + 2 (i % 2)),
+          // so thread t receives k pairs 8 cc + 2 (t % 4) (+ 1) of features 8 jj + t / 4: registers
+          // v[4 (4 h2 + cc) ..] = r0..r3 of tcgen05.st.16x256b.
+          const int mi = lane >> 3, ri = lane & 7;
+          const int kr = ((ri >> 1) << 2) + (ri & 1) + 2 * (mi & 1);
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int k0 = 2 * c, k1 = 2 * c + 1;
-            const uint32_t lo = lds_u16(hb + (uint32_t)(k0 * 128 + ((j ^ (k0 & 7)) << 4)));
-            const uint32_t hi = lds_u16(hb + (uint32_t)(k1 * 128 + ((j ^ (k1 & 7)) << 4)));
-            v[c] = lo | (hi << 16);
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int jj = 4 * q + 2 * h2 + (mi >> 1);
+            const uint32_t hb = base + (uint32_t)((jj >> 3) * 8192);
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              const int k = 16 * cc + kr;
+              ldsm_x4_trans(hb + (uint32_t)(k * 128 + (((jj & 7) ^ (k & 7)) << 4)), v + 4 * (4 * h2 + cc));
+            }
           }
         }
         // the stage goes back to the TMA (async proxy) only after these generic-proxy reads: without
@@ -470,7 +487,17 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
           }
         }
         tc_fence_after();
-        tmem_st32(trow + (uint32_t)(slot * 32), v);
+        if (!BWD) {
+          tmem_st32(trow + (uint32_t)(slot * 32), v);
+        } else {
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              const uint32_t* r = v + 4 * (4 * h2 + cc);
+              tmem_st_16x256b(trow + ((uint32_t)(16 * h2) << 16) + (uint32_t)(slot * 32 + 8 * cc), r[0], r[1], r[2], r[3]);
+            }
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
