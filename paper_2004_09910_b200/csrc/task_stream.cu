@@ -77,17 +77,12 @@ struct StCfg {
   static constexpr int OFF_RECV = OFF_ACT + KB_MAX * ATILE;
   static constexpr int OFF_BAR = OFF_RECV + NV * 2 * RECV;
   static constexpr int SMEM = OFF_BAR + 8192 + 1024;
-  // TMEM: NV x 2 accumulator buffers of 32 columns, then NSLOT weight slots of 32 columns
-#ifndef TGP_ST_ACC
-  static constexpr int ACC = NV * 64;
-#else
-  static constexpr int ACC = NV == 2 ? 128 : TGP_ST_ACC;
-#endif
-#ifndef TGP_ST_NSLOT
-  static constexpr int NSLOT = (512 - ACC) / 32;
-#else
-  static constexpr int NSLOT = TGP_ST_NSLOT;
-#endif
+  // TMEM: one accumulator of 32 columns per epilogue group, then NSLOT weight slots of 32 columns.
+  // A group's consecutive units are consecutive phases, and phase p + 1's activations exist only after
+  // every owner's epilogue of phase p -- which drained the accumulator first -- so a second
+  // accumulator buffer would never be used concurrently; its 32 columns hold one more weight slot.
+  static constexpr int ACC = NV * 32;
+  static constexpr int NSLOT = (512 - ACC) / 32;  // 15 (full grid) / 14 (half grid)
 };
 constexpr int ST_SMEM_MAX = StCfg<false, 1>::SMEM > StCfg<true, 2>::SMEM ? StCfg<false, 1>::SMEM : StCfg<true, 2>::SMEM;
 // warps: TMA, MMA, poller, NV epilogue groups of 4, 4 copy -> 352 (NV = 1) / 480 (NV = 2) threads
@@ -203,9 +198,9 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
   uint8_t* act = smem + Cfg::OFF_ACT;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);  // [NST] weight tile landed in the ring
   uint64_t* empty = full + 16;   // [NST] ring stage read by the copy warps (4 arrivals)
-  uint64_t* aempty = empty + 16; // [NSLOT / 2 <= 8] TMEM slot pair consumed by the MMAs (commit)
-  uint64_t* tfull = aempty + 8;  // [2 groups][2] TMEM accumulator ready
-  uint64_t* tempty = tfull + 4;  // [2][2] TMEM accumulator drained (128 arrivals)
+  uint64_t* aempty = empty + 16; // [NSLOT <= 16] TMEM weight slot consumed by the MMAs (commit)
+  uint64_t* tfull = aempty + 16; // [2 groups][2] TMEM accumulator ready (index 2 g)
+  uint64_t* tempty = tfull + 4;  // [2][2] TMEM accumulator drained (128 arrivals; index 2 g)
   uint64_t* rbar = tempty + 4;   // [2][2] split-K partials of a unit received (owner)
   uint64_t* bfull = rbar + 4;    // activation operand of the current phase landed (TMA)
   uint64_t* bempty = bfull + 1;  // activation operand consumed (commit after the phase's MMAs)
@@ -251,7 +246,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 4);
     }
-    for (int s = 0; s < NSLOT / 2; ++s) mbar_init(&aempty[s], 1);
+    for (int s = 0; s < NSLOT; ++s) mbar_init(&aempty[s], 1);
     for (int w = 0; w < 4; ++w) st_release_cta_u32(smem_u32(smem + OFF_BAR + 6160 + 4 * w), 0u);
     for (int b = 0; b < 4; ++b) {
       mbar_init(&tfull[b], 1);
@@ -369,14 +364,13 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
         const bool last = un >= NU || un / NV != p;
         const int nkb = phase_of(t, p).K / (SK * 64);
         const uint32_t idesc = ncol(p) == 32 ? idesc32 : idesc16;
-        const int buf = ng[grp] & 1, uu = ng[grp] >> 1;
-        mbar_wait(&tempty[grp * 2 + buf], (uint32_t)((uu & 1) ^ 1));
+        mbar_wait(&tempty[grp * 2], (uint32_t)((ng[grp] & 1) ^ 1));
         if (first) {
           mbar_wait(bfull, (uint32_t)(nload & 1));
           if constexpr (NV == 1) st_release_cta_u32(mstart, (uint32_t)(nload + 1));
         }
         tc_fence_after();
-        const uint32_t dacc = tmem + (uint32_t)(grp * 64 + buf * 32);
+        const uint32_t dacc = tmem + (uint32_t)(grp * 32);
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int slot = g % NSLOT;
           if (g >= ready) {
@@ -398,10 +392,10 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
           for (int kk = 0; kk < 4; ++kk)
             tc_mma_bf16_ts(dacc, ta + (uint32_t)(kk * 8), make_sdesc_sw128(b + kk * 32, 16, 1024), idesc,
                            (kb | kk) ? 1u : 0u);
-          if (slot & 1) tc_commit(&aempty[slot >> 1]);  // slots are released in pairs (one commit per 8 MMAs)
+          tc_commit(&aempty[slot]);  // the slot is free once its 4 MMAs completed
         }
         dbg_stamp(t, p, 4);
-        tc_commit(&tfull[grp * 2 + buf]);
+        tc_commit(&tfull[grp * 2]);
         if (last) {
           tc_commit(bempty);
           ++nload;
@@ -474,7 +468,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // the ring stage is free (the tile is in registers)
-        mbar_wait(&aempty[slot >> 1], (uint32_t)((rs & 1) ^ 1));
+        mbar_wait(&aempty[slot], (uint32_t)((rs & 1) ^ 1));
         if constexpr (NV == 1) {
           // full grid: a tile of a LATER phase waits while the current phase's MMAs run (its
           // tcgen05.st would share TMEM bandwidth with their A-operand reads; F task 512 -> 481 us);
@@ -593,15 +587,15 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
     auto gemm_result = [&](auto NC, float* acc, float* acc2) {
       const int buf = n & 1, u = n >> 1;
       constexpr int nc = decltype(NC)::value, nq = nc / 4;
-      mbar_wait(&tfull[g * 2 + buf], (uint32_t)(u & 1));
+      mbar_wait(&tfull[g * 2], (uint32_t)(n & 1));
       tc_fence_after();
       if (et == 0) dbg_stamp(t, cur_p, 5);
       float v[32];
-      const uint32_t ta = tmem + (uint32_t)(g * 64 + buf * 32) + ((uint32_t)(lg * 32) << 16);
+      const uint32_t ta = tmem + (uint32_t)(g * 32) + ((uint32_t)(lg * 32) << 16);
       tmem_ld16(ta, v);
       if constexpr (nc == 32) tmem_ld16(ta + 16, v + 16);
       tc_fence_before();
-      mbar_arrive(&tempty[g * 2 + buf]);
+      mbar_arrive(&tempty[g * 2]);
       const uint32_t rb = smem_u32(recv + buf * (RECV / 4));
       const uint32_t dbar = mapa_shared(smem_u32(&rbar[g * 2 + buf]), (uint32_t)lg);
 #pragma unroll
