@@ -81,8 +81,9 @@ struct StCfg {
   // A group's consecutive units are consecutive phases, and phase p + 1's activations exist only after
   // every owner's epilogue of phase p -- which drained the accumulator first -- so a second
   // accumulator buffer would never be used concurrently; its 32 columns hold one more weight slot.
-  static constexpr int ACC = NV * 32;
-  static constexpr int NSLOT = (512 - ACC) / 32;  // 15 (full grid) / 14 (half grid)
+  // (NCOLMAX columns: 16 rows forward, the backward's 32-row [u | n] dG operand)
+  static constexpr int ACC = NV * NCOLMAX;
+  static constexpr int NSLOT = (512 - ACC) / 32;  // 15, except 14 on the half grid of a backward task
 };
 constexpr int ST_SMEM_MAX = StCfg<false, 1>::SMEM > StCfg<true, 2>::SMEM ? StCfg<false, 1>::SMEM : StCfg<true, 2>::SMEM;
 // warps: TMA, MMA, poller, NV epilogue groups of 4, 4 copy -> 352 (NV = 1) / 480 (NV = 2) threads
@@ -191,7 +192,7 @@ template <bool BWD, int NV>
 __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const __grid_constant__ STask t) {
   using Cfg = StCfg<BWD, NV>;
   constexpr int NST = Cfg::NST, ATILE = Cfg::ATILE, RECV = Cfg::RECV, OFF_BAR = Cfg::OFF_BAR;
-  constexpr int NSLOT = Cfg::NSLOT, ACC = Cfg::ACC;
+  constexpr int NSLOT = Cfg::NSLOT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
@@ -263,8 +264,8 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
         if (u < NU) mbar_arrive_expect_tx(&rbar[g * 2 + b], recv_bytes(u));
       }
   }
-  // TMEM: group g, buffer b: columns [64 g + 32 b, + 32) (up to 32 fp32 accumulator columns);
-  // [ACC, 512): NSLOT weight slots of 32 columns
+  // TMEM: [0, 32 NSLOT): NSLOT weight slots of 32 columns; then group g's fp32 accumulator at
+  // 32 NSLOT + NCOLMAX g (16 or 32 columns)
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
           if constexpr (NV == 1) st_release_cta_u32(mstart, (uint32_t)(nload + 1));
         }
         tc_fence_after();
-        const uint32_t dacc = tmem + (uint32_t)(grp * 32);
+        const uint32_t dacc = tmem + (uint32_t)(NSLOT * 32 + grp * Cfg::NCOLMAX);
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int slot = g % NSLOT;
           if (g >= ready) {
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
           }
           if (kb == 0) dbg_stamp(t, p, 3);
           if (kb == nkb / 2) dbg_stamp(t, p, 10);
-          const uint32_t ta = tmem + (uint32_t)(ACC + slot * 32);
+          const uint32_t ta = tmem + (uint32_t)(slot * 32);
           const uint32_t b = act0 + (uint32_t)(kb * ATILE);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
@@ -411,7 +412,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
     // half = even k), the K-major A-in-TMEM layout of tcgen05.mma (tc_mma_bf16_ts).
     const int q = warp & 3, f = 32 * q + lane;
     const uint32_t copied = smem_u32(smem + OFF_BAR + 6160);  // [4] tiles this copy warp has in TMEM
-    const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)ACC;
+    const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
     const uint32_t ring0 = smem_u32(ring);
     int g = 0;
     int pord = -1, lastp = -1, dph = 0;  // loaded-phase ordinal of the tile, MMA-complete phases
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
       tc_fence_after();
       if (et == 0) dbg_stamp(t, cur_p, 5);
       float v[32];
-      const uint32_t ta = tmem + (uint32_t)(g * 32) + ((uint32_t)(lg * 32) << 16);
+      const uint32_t ta = tmem + (uint32_t)(NSLOT * 32 + g * Cfg::NCOLMAX) + ((uint32_t)(lg * 32) << 16);
       tmem_ld16(ta, v);
       if constexpr (nc == 32) tmem_ld16(ta + 16, v + 16);
       tc_fence_before();
