@@ -152,11 +152,14 @@ TGP_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 TGP_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-// 16 lanes x 256 bit: thread t writes lane t/4 (r0, r1) and lane t/4 + 8 (r2, r3), columns 2(t%4), +1
-TGP_DEV void tmem_st_16x256b(uint32_t taddr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
-  asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r0), "r"(r1), "r"(r2),
-               "r"(r3)
-               : "memory");
+// 16 lanes x 4 x 256 bit: per 8-column chunk c (registers 4c .. 4c + 3) thread t writes lane t/4
+// (r0, r1) and lane t/4 + 8 (r2, r3), columns 8c + 2(t%4), +1
+TGP_DEV void tmem_st_16x256b_x4(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
 }
 // four 8x8 b16 matrices, transposed: thread t gets {M[2(t%4)][t/4], M[2(t%4)+1][t/4]} of matrix i in
 // register i; threads 8i..8i+7 give the row addresses of matrix i
@@ -486,12 +489,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
           tmem_st32(trow + (uint32_t)(slot * 32), v);
         } else {
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2)
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-              const uint32_t* r = v + 4 * (4 * h2 + cc);
-              tmem_st_16x256b(trow + ((uint32_t)(16 * h2) << 16) + (uint32_t)(slot * 32 + 8 * cc), r[0], r[1], r[2], r[3]);
-            }
+          for (int h2 = 0; h2 < 2; ++h2) tmem_st_16x256b_x4(trow + ((uint32_t)(16 * h2) << 16) + (uint32_t)(slot * 32), v + 16 * h2);
         }
         tmem_st_wait();
         tc_fence_before();

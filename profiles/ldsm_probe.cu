@@ -1,4 +1,4 @@
-// Probe (diagnostics, not product code): does ldmatrix.x4.trans + tcgen05.st.16x256b move an MN-major
+// Probe (diagnostics, not product code): does ldmatrix.x4.trans + tcgen05.st.16x256b.x4 move an MN-major
 // 128-byte-swizzled bf16 tile ([64 k][64 f] halves) into the K-major A-in-TMEM layout (lane = feature,
 // column c = k pair (2c, 2c+1))?  Fills the tile with code(f, k), copies it with the product's address
 // arithmetic, reads TMEM back with tcgen05.ld.32x32b.x32 and compares on the host.
@@ -12,10 +12,12 @@
 
 using namespace tgp;
 
-__device__ void st16x256(uint32_t taddr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
-  asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r0), "r"(r1), "r"(r2),
-               "r"(r3)
-               : "memory");
+__device__ void st16x256x4(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
 }
 __device__ void ldsm4t(uint32_t a, uint32_t* r) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -56,12 +58,7 @@ __global__ void __launch_bounds__(128, 1) probe(uint32_t* out) {
   }
   const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
 #pragma unroll
-  for (int h2 = 0; h2 < 2; ++h2)
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      const uint32_t* r = v + 4 * (4 * h2 + cc);
-      st16x256(trow + ((uint32_t)(16 * h2) << 16) + (uint32_t)(8 * cc), r[0], r[1], r[2], r[3]);
-    }
+  for (int h2 = 0; h2 < 2; ++h2) st16x256x4(trow + ((uint32_t)(16 * h2) << 16), v + 16 * h2);
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   tc_fence_before();
   __syncthreads();
