@@ -54,6 +54,8 @@ struct TcCfg {
   static constexpr int BAR_OFF = DATA + RECV_BYTES + (PUSH ? CS_BYTES : 0);
   static constexpr int SMEM = BAR_OFF + 1024 + 256;
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  // the push epilogue stages the whole partial tile in the (idle) pipeline buffers
+  static_assert(!PUSH || RED_BYTES <= STAGES * STAGE, "split-K staging must fit the pipeline buffers");
 };
 
 TGP_DEV void tma_store_2d(const void* desc, const void* smem, int32_t c0, int32_t c1, bool reduce_add) {
