@@ -7,8 +7,8 @@ measured.  Model (clock-cycle schedule, Alg. 1, mirrored
   t_BF'(n) = the paired B + F' task (both half grids, R5) per block x (32 / n) + c
   h        = per-clock hand-off: fused-send flag + the consumer's stream wait (one-way; half the CE
              ping-pong of profiles/round2_transport_sweep.txt as an upper bound)
-c is fitted from the n = 1 phase timeline (F task = 64 phases x 8.2 us + c).
-    python profiles/predict_e8.py profiles/r5/<bench>.json"""
+c is fitted from the n = 1 phase timeline (F task = 64 phases x phase period + c).
+    python profiles/predict_e8.py profiles/<round>/<bench>.json [phase_us]"""
 import json
 import sys
 
@@ -18,7 +18,7 @@ m, blocks = 32, 32
 T1 = b["ms_per_step"] * 1e3
 tF1, tB1 = tasks["F"]["median_us"], tasks["B"]["median_us"]  # B = the paired B task (lane 0)
 tW = tasks["W"]["median_us"]
-phase = 8.2
+phase = float(sys.argv[2]) if len(sys.argv) > 2 else 8.2  # measured F-task phase period (stamps)
 c = max(tF1 - 2 * blocks * phase, 0.0)
 fold = 450.0
 h = 11.5 / 2  # one-way hand-off, CE ping-pong / 2 (the fused flag is cheaper)
