@@ -2,9 +2,10 @@
 //
 //   dW[m][n] (=|+=) sum_k A[k][m] * B[k][n]      A = dY^T-operand [K rows][M], B = X [K rows][N] (bf16)
 //
-// K = the mini-batch rows (512 at C2), M = N = 4096.  One CTA per SM loops over 128 x 256 output
-// tiles (static round-robin: 512 tiles on 148 SMs at C2; measured over 128 x 128 on the C5 8-layer
-// step: 58.0 -> 57.4 ms, profiles/r7/r7w_summary.txt), TMA -> 4-stage shared-memory ring ->
+// K = the mini-batch rows (512 at C2), M = N = 4096.  One CTA per SM loops over 128 x 128 output
+// tiles (static round-robin: 1024 tiles on 148 SMs, <= 7 each), TMA -> 5-stage shared-memory ring ->
+// (128 x 256 tiles, TGP_DW_BN=256, measured 1 % faster on C5 but hit intermittent illegal-address
+// faults with two partitions on one device, profiles/r7/r8d_summary.txt -- not used)
 // tcgen05.mma (both operands MN-major SW128, fp32 in TMEM) with TMEM double-buffered across tiles,
 // so tile t+1's loads and MMAs overlap tile t's epilogue.  Epilogue: TMEM -> 128-byte-swizzled
 // shared-memory chunk -> TMA tensor store (first backward after a step) or TMA reduce-add
@@ -20,7 +21,7 @@ namespace tgp {
 
 namespace {
 #ifndef TGP_DW_BN
-#define TGP_DW_BN 256
+#define TGP_DW_BN 128
 #endif
 constexpr int DW_BM = 128, DW_BN = TGP_DW_BN, DW_BK = 64;
 constexpr int DW_STAGE = (DW_BM + DW_BN) * DW_BK * 2;  // 32 KB

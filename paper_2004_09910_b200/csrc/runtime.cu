@@ -1215,7 +1215,26 @@ static int issue_task(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<
       // so it is hoisted onto lane 1 and runs beside B_{i,j}, both on half grids; issued before B's
       // gradient wait so it does not wait for the downstream partition
       bool paired = false;
-      if (rc.kind == K_B && stream_task && s.pair_ok && c->pair && c->order_seed == 0 && i >= 2 &&
+      if (rc.kind == K_B && !stream_task && s.pair_layer && c->pair && c->order_seed == 0 && !c->relay &&
+          !c->abl_streams && i >= 2 &&
+          checkpointed(i - 1, c->m, c->ckpt) && !s.hoisted[i - 1]) {
+        // per-layer partitions: the same hoist with full-size kernels on lane 1 (exec_forward launches
+        // on s.comp, so the lanes are swapped around its issue / graph capture)
+        int pr0 = 0, pM = 0;
+        micro_rows(c, B, i - 1, &pr0, &pM);
+        TGP_CUDA_TRY(cudaEventRecord(s.ev_pair, s.comp));  // after B_{i+1,j}, the last reader of the slot
+        TGP_CUDA_TRY(cudaStreamWaitEvent(s.comp2, s.ev_pair, 0));
+        cudaEvent_t tr = nullptr;
+        trace_begin(c, s, s.comp2, 3, K_RECOMPUTE, i - 1, &tr);
+        std::swap(s.comp, s.comp2);
+        const int rcode = run_task(c, s, s.gR2[i - 2], B, [&] { return exec_forward(c, s, i - 1, pr0, pM); }, s.comp);
+        std::swap(s.comp, s.comp2);
+        TGP_TRY(rcode);
+        trace_end(c, s, s.comp2, 3, K_RECOMPUTE, i - 1, tr);
+        TGP_CUDA_TRY(cudaEventRecord(s.rdone[i - 2], s.comp2));
+        s.hoisted[i - 1] = 1;
+      }
+      if (rc.kind == K_B && stream_task && s.pair_ok && !s.pair_layer && c->pair && c->order_seed == 0 && i >= 2 &&
           checkpointed(i - 1, c->m, c->ckpt) && !s.hoisted[i - 1]) {
         int pr0 = 0, pM = 0;
         micro_rows(c, B, i - 1, &pr0, &pM);

@@ -131,6 +131,7 @@ struct Stage {
   // lane 0, both on a half grid (st_half clusters, two output slabs each); lane 1 has its own
   // counters / statistics scratch.  Checkpointed micro-batches alternate two scratch slots.
   bool pair_ok = false;
+  bool pair_layer = false;  // pairing with per-layer kernels (no stream kernel): F' on comp2, full-size grids
   int st_half = 0;
   cudaStream_t comp2 = nullptr;
   unsigned* st_cnt2 = nullptr;

@@ -1,7 +1,7 @@
 """GPU tests of F' / B pairing (option "pair_recompute", runtime.cu issue()): the recompute F'_{i-1,j}
 depends only on the stage input and the weights, not on B_{i,j}, so it runs on
-a second compute lane beside B_{i,j}, both persistent task kernels on half grids (each cluster owns
-two output slabs).
+a second compute lane beside B_{i,j}: persistent task kernels on half grids (each cluster owns two
+output slabs), or -- on partitions that run the per-layer kernels -- full-size kernels sharing the SMs.
 
 * Results are BITWISE equal with and without pairing (a half-grid task computes every output with the
   same split-K order and fixed-order reductions as the full grid; reading Z21), over checkpoint
@@ -52,6 +52,19 @@ def test_pairing_bitwise_d_ne_h_ragged(d, H):
 
 def test_pairing_bitwise_full_c2_width():
     _both(C.resmlp_stack(4, 4096), 512, 32, 1, "except_last", steps=1)
+
+
+@pytest.mark.parametrize("ckpt", ["except_last", "always"])
+def test_pairing_bitwise_per_layer_kernels(ckpt):
+    # 64-row micro-batches: the per-layer tcgen05 GEMMs (no stream kernel); F'_{i-1} runs on lane 1
+    # with full-size kernels beside B_i, two partitions on one device
+    _both(C.resmlp_stack(4, 512, hidden=1024, dropout=0.1), 256, 4, 2, ckpt)
+
+
+def test_pairing_bitwise_per_layer_portals():
+    # a U-MLP with skip routes (MERGE layers pop the portal tensors in F and F'); the GPT-2-shaped stack
+    # is covered by test_gpu_gpt2.py::test_c5_checkpoint_modes_bitwise (paired always / except_last == never)
+    _both(C.umlp(d=256, levels=2, blocks_per_level=1, mid_blocks=1), 64, 2, 2, "always")
 
 
 def test_pairing_dependencies_on_the_device_timeline():
