@@ -69,6 +69,9 @@ def main():
         P = Pipeline(layers, chunks=a.chunks, devices=[0] * a.parts, balance=bal, checkpoint=a.ckpt, max_batch=B, dtype="bf16",
                      seed=1)
         P.init_params(1)
+        # F'/B pairing is this implementation's addition, not one of the paper's Table 1 components:
+        # off in every arm so the rows compare the paper's design against its ablations
+        P.set_option("pair_recompute", 0)
         for k, v in opts.items():
             P.set_option(k, v)
 
