@@ -288,6 +288,8 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *             (default 1; 0 = the one-tile-per-CTA GEMM)
  *  "attn_tc"  PROCESS-WIDE: 1 = tcgen05 attention forward where seq % 128 == 0, 0 = mma.sync,
  *             -1 = the TGP_ATTN_TC environment default (off)
+ *  "dead_stash"  1 (default): the stream-kernel F task of a checkpointed micro-batch stores only its
+ *                 output (F' recomputes the intermediates before B reads them); 0: it stores them too
  *  "nvtx"        1 (default): NVTX ranges per tgp_forward / tgp_backward call and per issued task
  *                 (named after its schedule record, e.g. "F i=3 j=2"); 0: none
  *  "watchdog_ms" bound on the host wait for a call's device work (forward / backward), ms

@@ -336,7 +336,7 @@ static int st_refold(tgp_ctx* c, Stage& s, int B) {
 // lane: 0 = full grid on comp; 1 = half grid on comp (a paired B); 2 = half grid on comp2 with the
 // lane-1 counters / statistics (a paired F', beside the lane-1 B)
 static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd, int lane = 0, float* send_to = nullptr,
-                            uint32_t* send_flag = nullptr) {
+                            uint32_t* send_flag = nullptr, bool keep = true) {
   const LayerRT& L0 = c->layers[s.l0];
   STask t{};
   t.L = s.l1 - s.l0;
@@ -362,6 +362,7 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
   t.cnt = lane == 2 ? s.st_cnt2 : s.st_cnt;
   t.seed = c->seed;
   t.step = s.dstep;
+  t.keep = keep ? 1 : 0;
   t.sleep_ns = c->st_sleep_ns;
   t.inflight = c->st_inflight;
   if (lane == 0 && getenv("TGP_ST_DEBUG")) {  // diagnostics: per-CTA, per-phase %globaltimer stamps
@@ -391,8 +392,8 @@ static int ln_bwd_any(tgp_ctx* c, Stage& s, bool pdl, const float* dh, const flo
   return 0;
 }
 
-static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M) {
-  if (use_stream(c, s, M)) return exec_task_stream(c, s, i, r0, M, false);
+static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M, bool keep = true) {
+  if (use_stream(c, s, M)) return exec_task_stream(c, s, i, r0, M, false, 0, nullptr, nullptr, keep);
   const int slot = c->slot_of[i];
   float* x = s.self.fwd_in + (size_t)r0 * s.d_in;
   bool first_kernel = true;
@@ -1282,6 +1283,9 @@ static int issue_task(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<
         send_to = c->view[nb].grad_in + (size_t)r0 * s.d_in;
         send_flag = flag_grad(c, c->view[nb], i);
       }
+      // a checkpointed F keeps only its output (F' recomputes the intermediates before B reads them;
+      // F and F' have separate task graphs)
+      const bool f_keep = !(rc.kind == K_F && checkpointed(i, c->m, c->ckpt) && c->dead_stash);
       cudaEvent_t ta = nullptr;
       trace_begin(c, s, s.comp, 0, rc.kind, i, &ta);
       if (rc.kind == K_B && (paired || send)) {
@@ -1294,12 +1298,12 @@ static int issue_task(tgp_ctx* c, const Rec& rc, int B, std::vector<std::vector<
         TGP_CUDA_TRY(cudaEventRecord(s.bdone[i - 1], s.comp));
       } else if (send) {  // F_{i,j} sending its output
         TGP_TRY(run_task(c, s, s.gF[i - 1], B,
-                         [&] { return exec_task_stream(c, s, i, r0, M, false, 0, send_to, send_flag); }, nullptr, 1));
+                         [&] { return exec_task_stream(c, s, i, r0, M, false, 0, send_to, send_flag, f_keep); }, nullptr, 1));
         TGP_CUDA_TRY(cudaEventRecord(s.fdone[i - 1], s.comp));
       } else {
         // F without a send, or F' (never sends; with a sending F it has its own graph)
-        TaskGraph& tg = (rc.kind == K_RECOMPUTE && fuse_fwd(c, s, M)) ? s.gR[i - 1] : s.gF[i - 1];
-        TGP_TRY(run_task(c, s, tg, B, [&] { return exec_forward(c, s, i, r0, M); }));
+        TaskGraph& tg = rc.kind == K_RECOMPUTE ? s.gR[i - 1] : s.gF[i - 1];
+        TGP_TRY(run_task(c, s, tg, B, [&] { return exec_forward(c, s, i, r0, M, rc.kind == K_RECOMPUTE || f_keep); }));
         if (rc.kind == K_F) TGP_CUDA_TRY(cudaEventRecord(s.fdone[i - 1], s.comp));
       }
       trace_end(c, s, s.comp, 0, rc.kind, i, ta);

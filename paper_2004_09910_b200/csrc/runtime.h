@@ -225,6 +225,7 @@ struct tgp_ctx {
   bool connected = true;
   // asynchronous stream-ordered calls (tgp_*_async): the caller's stream while such a
   // call is being issued, and the event its work is ordered after (created on the stream's device)
+  bool dead_stash = true;  // stream-kernel F of a checkpointed micro-batch skips its dead intermediates (option "dead_stash")
   bool nvtx = true;  // NVTX ranges per call and per issued task (option "nvtx")
   bool async_call = false;
   cudaStream_t ustream = nullptr;

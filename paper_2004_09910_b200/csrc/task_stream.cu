@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
         rmp[rr] = l == 0 ? mu : rmu[rr];  // block 0: operand centred on its exact mean
         rmu[rr] = mu;
         rrs[rr] = rs;
-        if (blockIdx.x == 0 && g == 0 && rr < M) {
+        if (t.keep && blockIdx.x == 0 && g == 0 && rr < M) {
           t.micro[l].mean[rr] = mu;
           t.micro[l].rstd[rr] = rs;
         }
@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = 4 * ew + e;
-        if (r < M) t.micro[l].hop[(size_t)r * d + fo] = __float2bfloat16_rn(gm * ((y[e] - rmu[r]) * rrs[r]) + b);
+        if (t.keep && r < M) t.micro[l].hop[(size_t)r * d + fo] = __float2bfloat16_rn(gm * ((y[e] - rmu[r]) * rrs[r]) + b);
       }
     };
 
@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
           // read only by the backward task / W_j: stored off the critical path
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (4 * ew + e < M) aout[(size_t)(4 * ew + e) * H + fo] = acc[e];
+            if (t.keep && 4 * ew + e < M) aout[(size_t)(4 * ew + e) * H + fo] = acc[e];
         } else if (own_d) {
           ln_rows(l);
         }
@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
           // the residual stream is read by this thread (next block) and later tasks only
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (4 * ew + e < M) yout[(size_t)(4 * ew + e) * d + fo] = yk[e];
+            if ((t.keep || l + 1 == t.L) && 4 * ew + e < M) yout[(size_t)(4 * ew + e) * d + fo] = yk[e];
         }
       }
     } else {

@@ -72,6 +72,10 @@ struct STask {
   float* y_send;
   uint32_t* send_flag;
   const uint32_t* send_seq;  // device copy of the call sequence number (graph replays read it)
+  int keep;           // forward: 1 = store the block intermediates (pre-activation a, LN-output stash, block
+                      // outputs, LN statistics); 0 = a checkpointed F, whose intermediates F' recomputes
+                      // before B reads them (a checkpointed F keeps only the stage input) -- only
+                      // the stage output is stored
   unsigned sleep_ns;  // back-off between dependency polls
   unsigned inflight;  // max weight tiles issued but not landed per CTA (0 = limited by the ring only)
 };
