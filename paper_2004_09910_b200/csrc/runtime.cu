@@ -377,7 +377,8 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
   return task_stream_launch(lane == 2 ? s.comp2 : s.comp, t, lane ? s.st_half : s.st_clusters);
 }
 
-// F_{i,j} (and F'_{i,j}: identical kernels and launch configuration -> bitwise identical output)
+// F_{i,j} (and F'_{i,j}: identical kernels and launch configuration -> bitwise identical output).
+// keep = false: a checkpointed F, whose backward-only intermediates (pre-activations) F' recomputes
 // LayerNorm backward dx = dy + LN_bwd(dh) (dy nullable) with the per-16-row column partials.
 static int ln_bwd_any(tgp_ctx* c, Stage& s, bool pdl, const float* dh, const float* x, const float* mean,
                       const float* rstd, const float* gamma, const float* dy, float* dx, int M, int d, float* pg,
@@ -421,7 +422,7 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M, bool keep = 
         e.mode = EPI_LINEAR_FWD;
         e.act = L.L.act;
         e.bias = mparam(s, L, 1);
-        e.zbuf = (L.L.act != TGP_ACT_NONE) ? L.z[slot] : nullptr;
+        e.zbuf = (L.L.act != TGP_ACT_NONE && keep) ? L.z[slot] : nullptr;  // pre-activation: backward only
         e.ldz = dout;
         e.out0 = y;
         e.ld0 = dout;
@@ -453,7 +454,7 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M, bool keep = 
         e1.mode = EPI_LINEAR_FWD;
         e1.act = L.L.act;
         e1.bias = mparam(s, L, 3);
-        e1.zbuf = L.z[slot];
+        e1.zbuf = keep ? L.z[slot] : nullptr;
         e1.ldz = H;
         e1.op = opptr(c, L.Gop, r0, H);
         e1.ld_op = H;
@@ -541,7 +542,7 @@ static int exec_forward(tgp_ctx* c, Stage& s, int i, int r0, int M, bool keep = 
         e3.mode = EPI_LINEAR_FWD;
         e3.act = TGP_ACT_GELU;
         e3.bias = mparam(s, L, 9);
-        e3.zbuf = L.z[slot];
+        e3.zbuf = keep ? L.z[slot] : nullptr;
         e3.ldz = H;
         e3.op = opptr(c, L.Gop, r0, H);
         e3.ld_op = H;
