@@ -20,12 +20,12 @@ from _gpu import gpu_step, make_case
 pytestmark = pytest.mark.gpu
 
 
-def _both(layers, B, m, n, ckpt, seed=4, steps=2):
+def _both(layers, B, m, n, ckpt, seed=4, steps=2, option="pair_recompute"):
     x, t, params = make_case(layers, B, seed, "bf16")
     res = {}
     for pair in (0, 1):
         g, P = gpu_step(layers, params, x, t, m=m, n=n, ckpt=ckpt, dtype="bf16", lr=0.05, seed=seed,
-                        options={"pair_recompute": pair}, steps=steps)
+                        options={option: pair}, steps=steps)
         res[pair] = g if steps > 1 else [g]
         P.close()
     for a, b in zip(res[0], res[1]):
@@ -65,6 +65,14 @@ def test_pairing_bitwise_per_layer_portals():
     # a U-MLP with skip routes (MERGE layers pop the portal tensors in F and F'); the GPT-2-shaped stack
     # is covered by test_gpu_gpt2.py::test_c5_checkpoint_modes_bitwise (paired always / except_last == never)
     _both(C.umlp(d=256, levels=2, blocks_per_level=1, mid_blocks=1), 64, 2, 2, "always")
+
+
+@pytest.mark.parametrize("rows", [64, 256])
+def test_checkpointed_f_without_dead_stores_is_bitwise(rows):
+    # option "dead_stash": a checkpointed F stores only its output (F' recomputes the intermediates):
+    # bitwise equal to storing everything, on the stream kernel (16-row micro-batches) and the
+    # per-layer kernels (64-row micro-batches)
+    _both(C.resmlp_stack(4, 512, hidden=1024, dropout=0.1), rows, 4, 2, "always", option="dead_stash")
 
 
 def test_pairing_dependencies_on_the_device_timeline():
