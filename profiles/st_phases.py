@@ -59,3 +59,23 @@ for p in range(NP):
     print(f"p{p:2d} W-first@{(base - t0) / 1e3:8.2f} us {per} | " + " ".join(r.replace(' ', '=', 1) for r in row))
 end = max(ev[:, :, 7].max(), ev[:, :, 4].max())
 print(f"total {(end - t0) / 1e3:.1f} us -> {(end - t0) / 1e3 / NP:.2f} us per GEMM phase")
+# per-CTA lag (which CTAs set the phase time): mean over phases of (MMA done - phase median), top 12
+if int(opts.get("lag", 0)):
+    lag = np.zeros(G)
+    wl = np.zeros(G)
+    for p in range(NP):
+        v = ev[:, p, 4].astype(np.float64)
+        w = ev[:, p, 2].astype(np.float64)
+        ok = v > 0
+        if ok.sum() < G // 2:
+            continue
+        lag += np.where(ok, v - np.median(v[ok]), 0.0)
+        wl += np.where(w > 0, w - np.median(w[w > 0]), 0.0)
+    lag /= NP
+    wl /= NP
+    order = np.argsort(-lag)
+    print("CTA (cluster, rank): mean MMA-done lag us / mean last-weight-tile lag us")
+    for cta in order[:12]:
+        print(f"  cta {cta:3d} (cluster {cta // 4:2d}, rank {cta % 4}): {lag[cta] / 1e3:6.2f} / {wl[cta] / 1e3:6.2f}")
+    print("lag by rank:", [round(float(lag[r::4].mean()) / 1e3, 2) for r in range(4)])
+    print("lag by cluster (first 32):", [round(float(lag[4 * c:4 * c + 4].mean()) / 1e3, 1) for c in range(G // 4)])
