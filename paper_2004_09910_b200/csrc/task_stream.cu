@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
         mbar_wait(&tempty[grp * 2], (uint32_t)((ng[grp] & 1) ^ 1));
         if (first) {
           mbar_wait(bfull, (uint32_t)(nload & 1));
-          if constexpr (NV == 1) st_release_cta_u32(mstart, (uint32_t)(nload + 1));
+          if constexpr (NV == 1 && !BWD) st_release_cta_u32(mstart, (uint32_t)(nload + 1));
         }
         tc_fence_after();
         const uint32_t dacc = tmem + (uint32_t)(NSLOT * 32 + grp * Cfg::NCOLMAX);
@@ -473,11 +473,14 @@ __global__ void __launch_bounds__(st_threads<NV>(), 1) task_stream_kernel(const 
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // the ring stage is free (the tile is in registers)
         mbar_wait(&aempty[slot], (uint32_t)((rs & 1) ^ 1));
-        if constexpr (NV == 1) {
-          // full grid: a tile of a LATER phase waits while the current phase's MMAs run (its
+        if constexpr (NV == 1 && !BWD) {
+          // full-grid forward: a tile of a LATER phase waits while the current phase's MMAs run (its
           // tcgen05.st would share TMEM bandwidth with their A-operand reads; F task 512 -> 481 us);
           // tiles of the running phase go at once.  Not on the half grid of a paired task, whose 32
-          // tiles per phase need every copy slot (measured: paired F' + B 976 -> 1196 us).
+          // tiles per phase need every copy slot (measured: paired F' + B 976 -> 1196 us), and not in
+          // the backward, whose heavier tile copies leave a CTA that fell behind no way to catch up:
+          // one straggler CTA per launch, 2.5-3 us late in every phase (B 582 -> 517 us without it,
+          // profiles/r7/r8p_summary.txt)
           while (true) {
             const int st = (int)ld_acquire_cta_u32(mstart);
             while (dph < st && mbar_test_wait(smem_u32(bempty), (uint32_t)(dph & 1))) ++dph;
