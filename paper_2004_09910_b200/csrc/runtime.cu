@@ -365,7 +365,10 @@ static int exec_task_stream(tgp_ctx* c, Stage& s, int i, int r0, int M, bool bwd
   t.keep = keep ? 1 : 0;
   t.sleep_ns = c->st_sleep_ns;
   t.inflight = c->st_inflight;
-  if (lane == 0 && getenv("TGP_ST_DEBUG")) {  // diagnostics: per-CTA, per-phase %globaltimer stamps
+  // diagnostics: per-CTA, per-phase %globaltimer stamps of the full-grid tasks (TGP_ST_DEBUG=1) or of the
+  // paired backward task on lane 1 (TGP_ST_DEBUG=2; half grid, the two units of a phase share a record)
+  const char* dbg_env = getenv("TGP_ST_DEBUG");
+  if (dbg_env && ((lane == 0 && atoi(dbg_env) != 2) || (lane == 1 && atoi(dbg_env) == 2))) {
     const size_t nd = (size_t)s.st_clusters * 4 * 2 * t.L * ST_DBG_SLOTS;
     if (!s.st_dbg) {
       TGP_CUDA_TRY(cudaMalloc(&s.st_dbg, nd * 8));

@@ -19,7 +19,11 @@ opts = dict(a.split("=") for a in sys.argv[1:])
 blocks = int(opts.get("blocks", 4))
 bwd = int(opts.get("bwd", 0))
 layers = C.resmlp_stack(blocks, 4096)
-P = Pipeline(layers, chunks=32, devices=[0], balance=[blocks], checkpoint="never", max_batch=512, dtype="bf16", seed=1)
+paired = int(opts.get("paired", 0))  # 1: stamps of the last PAIRED backward task (except_last, lane 1, half grid)
+if paired:
+    os.environ["TGP_ST_DEBUG"] = "2"
+P = Pipeline(layers, chunks=32, devices=[0], balance=[blocks], checkpoint="except_last" if paired else "never",
+             max_batch=512, dtype="bf16", seed=1)
 P.set_option("stream_poll_ns", int(opts.get("poll", 32)))
 P.set_option("stream_inflight", int(opts.get("inflight", 0)))
 P.set_option("graphs", 0)
@@ -40,6 +44,9 @@ buf = np.zeros(n.value, dtype=np.uint64)
 L.tgp_debug_stream_read(P.h, 0, buf.ctypes.data, n.value, ctypes.byref(n))
 NP = 2 * blocks
 G = n.value // (NP * 13)
+if paired:  # half grid: only the first G / 2 CTAs write
+    G //= 2
+    buf = buf[: G * NP * 13]
 ev = buf.reshape(G, NP, 13).astype(np.int64)
 names = ["B issue", "W first", "W last", "B landed", "MMA done", "TMEM rdy", "partials", "signal", "stats", "sig entry", "MMA half", "cp last", "bar passed"]
 t0 = ev[:, 0, 1].min()
