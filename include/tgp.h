@@ -306,8 +306,10 @@ tgp_status tgp_kernel_count(tgp_ctx* ctx, int64_t* n);
  *             neighbour partition's receive slab and release-stores the flag itself at system
  *             scope: compute fused with send, no copy kernel.  Off
  *             under the ablations and the transport negative controls.  Bitwise identical results.
- *  "pair_recompute" 1 (default) = F'_{i-1,j} runs on a second lane beside B_{i,j}, both stream
- *             tasks on half grids (F' depends only on the stage input); 0 = in place.
+ *  "pair_recompute" 1 (default) = F'_{i-1,j} runs on a second lane beside B_{i,j} (F' depends only
+ *             on the stage input): both stream-kernel tasks on half grids, or -- partitions on
+ *             the per-layer kernels -- full-size kernels sharing the SMs (bf16, not under the
+ *             ablate_portals / ablate_copy_streams toggles); 0 = in place.  Results are bitwise equal.
  * Table 1 ablation toggles (results are bitwise those of the default -- only the
  * issue order and the copy path change).  Need every partition in this process, and not between
  * forward and backward (TGP_E_UNSUPPORTED / TGP_E_STATE):
